@@ -1,0 +1,151 @@
+/*
+ * lre_b200.h — C ABI of the B200-native LRE (linear-regression-estimation)
+ * hot path of arXiv 1602.08604: Pauli outcome counts -> theta -> mu.
+ *
+ * Every pointer marked (device) is device memory owned by the caller; every
+ * call is asynchronous on the given cudaStream_t (pass 0 for the legacy
+ * stream) and returns an lre_status.  The library allocates nothing and keeps
+ * no hidden state except a launch counter.  Host code (Python via ctypes, see
+ * INTEGRATION.md) owns memory, streams and the NCCL communicator.
+ *
+ * Layout conventions (reference pauli.py:1-13): qubit 1 is the most
+ * significant digit/bit everywhere; counts are row-major (3^n settings, 2^n
+ * outcomes); theta is either NATURAL (index = base-4 Pauli digits I,X,Y,Z) or
+ * MASK_MAJOR (index = m * 2^n + a, m = X|Y mask, a = Y|Z mask).
+ */
+#ifndef LRE_B200_H
+#define LRE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *lre_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    LRE_OK = 0,
+    LRE_EINVAL = 1,       /* bad argument; maps to Python ValueError           */
+    LRE_ECUDA = 2,        /* CUDA launch/runtime failure; RuntimeError         */
+    LRE_ENOMEM = 3,       /* workspace too small; MemoryError                  */
+    LRE_EUNSUPPORTED = 4, /* size/dtype not supported by this build            */
+    LRE_EOVERFLOW = 5     /* shots too large for the requested count dtype     */
+} lre_status;
+
+typedef enum { LRE_U8 = 1, LRE_U16 = 2, LRE_I32 = 3, LRE_I64 = 4 } lre_dtype;
+
+typedef enum { LRE_LAYOUT_NATURAL = 0, LRE_LAYOUT_MASK_MAJOR = 1 } lre_layout;
+
+typedef enum {
+    LRE_OUT_THETA_F64 = 0, /* finished theta (fp64), requires the full setting range */
+    LRE_OUT_NUM_I64 = 1    /* exact int64 numerators N_i (partial sums allowed)     */
+} lre_out_kind;
+
+typedef enum {
+    LRE_STATE_MAXMIXED = 0,
+    LRE_STATE_GHZ = 1,
+    LRE_STATE_PRODUCTZ = 2,
+    LRE_STATE_W = 3
+} lre_state_kind;
+
+/* Human-readable status text. */
+const char *lre_strerror(int status);
+
+/* ABI version (major*100 + minor). */
+int lre_version(void);
+
+/* Number of kernels this library has launched since load (for benchmarking). */
+int64_t lre_launch_count(void);
+
+/*
+ * Step (i) workspace size in bytes for settings [w_begin, w_end).
+ * Replaces the per-worker private 4^n partials of
+ * reference pipeline.py:74-90,128-137 (step_one_least_squares).
+ */
+int lre_step1_workspace(int n, int64_t shots, int64_t w_begin, int64_t w_end, size_t *bytes);
+
+/*
+ * Step (i): counts (device, rows = settings [w_begin, w_end), 2^n columns,
+ * dtype `count_dtype`) -> `out` (device).
+ *   out_kind == LRE_OUT_THETA_F64: out = double[4^n] theta (needs the full
+ *     range [0, 3^n)); theta_i = N_i / shots * 2^{-n/2} / 3^{zc(i)}.
+ *   out_kind == LRE_OUT_NUM_I64: out = int64[4^n] exact numerators of this
+ *     setting range (summable across ranges/devices).
+ * Replaces reference pipeline.py:116-138 (step_one_least_squares) together
+ * with _kernels.py:34-56 (accumulate_fast) and pauli.py:153-209.
+ * w_begin/w_end must be multiples of lre_shard_quantum(n) (except w_end = 3^n).
+ */
+int lre_step1(const void *counts, int count_dtype, int n, int64_t shots, int64_t w_begin,
+              int64_t w_end, void *workspace, size_t workspace_bytes, void *out, int out_kind,
+              int layout, lre_stream_t stream);
+
+/* Alignment quantum of setting shards for lre_step1 (3^q1 of the first pass). */
+int64_t lre_shard_quantum(int n);
+
+/* Number of fold passes step (i) runs at this size (1 for n <= 7). */
+int lre_step1_num_passes(int n, int64_t shots);
+
+/*
+ * Streaming form of lre_step1 for records that arrive in setting chunks
+ * (host records larger than HBM, pipelined H2D): lre_step1_stage runs the
+ * first fold pass of chunk [w_begin, w_end) (rows of `counts`) into a
+ * full-range workspace (size from lre_step1_workspace(n, shots, 0, 3^n));
+ * after every chunk has been staged once, lre_step1_finish runs the remaining
+ * passes.  Requires lre_step1_num_passes(n, shots) >= 2.
+ */
+int lre_step1_stage(const void *counts, int count_dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end,
+                    void *workspace, size_t workspace_bytes, lre_stream_t stream);
+int lre_step1_finish(void *workspace, size_t workspace_bytes, int n, int64_t shots, void *out, int out_kind,
+                     int layout, lre_stream_t stream);
+
+/*
+ * int64 numerators (device, entries [begin, end) of `layout`) -> fp64 theta
+ * (device, same positions).  Epilogue of reference pipeline.py:138 and
+ * records.py:62-64 (frequencies = counts / float(shots)).
+ */
+int lre_finalize(const int64_t *num, int n, int64_t shots, int layout, int64_t begin, int64_t end,
+                 double *theta, lre_stream_t stream);
+
+/* theta relayout NATURAL <-> MASK_MAJOR (device -> device, out of place). */
+int lre_theta_relayout(const double *src, int src_layout, int n, double *dst, lre_stream_t stream);
+
+/*
+ * Step (ii): theta (device, MASK_MAJOR slice holding masks [m_begin, m_end):
+ * theta_mm[(m - m_begin)*2^n + a]) -> mu (device, complex128
+ * as interleaved doubles).  S = m_end - m_begin must be a power of two and
+ * m_begin a multiple of S; mu is written as d rows x S columns:
+ *   mu_out[r*S + c] = mu[r, ((r / S) ^ (m_begin / S)) * S + c]
+ * (S = 2^n gives the full row-major matrix).  Replaces reference
+ * pipeline.py:141-161 (step_two_assemble) and pauli.py:270-297.
+ */
+int lre_assemble(const double *theta_mm, int n, int64_t m_begin, int64_t m_end, double *mu_out,
+                 lre_stream_t stream);
+
+/*
+ * Record validation (reference records.py:34-56, MeasurementRecord.validate):
+ * result (device int64[3]) receives {first row whose sum != shots (or
+ * INT64_MAX), that row's sum, minimum count value}.
+ */
+int lre_validate_counts(const void *counts, int count_dtype, int n, int64_t rows, int64_t shots,
+                        int64_t *result, lre_stream_t stream);
+
+/*
+ * Device synthetic count generator (north-star item 4; reference
+ * simulate.py:167-266).  Rows [w_begin, w_end) of the record of state
+ * `kind` (bits = productz basis string) are written to out (device, row 0 =
+ * setting w_begin).  exact != 0 writes the noiseless dyadic record
+ * (shots must equal 2^n; LRE_EINVAL if the state is not dyadic).
+ * Sampling draws `shots` outcomes per setting from a Philox4x32-10 stream
+ * keyed on (seed, setting), so records do not depend on sharding.
+ */
+int lre_generate_counts(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, int exact,
+                        int64_t w_begin, int64_t w_end, void *out, int count_dtype,
+                        lre_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LRE_B200_H */

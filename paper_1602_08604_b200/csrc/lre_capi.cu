@@ -1,0 +1,154 @@
+// C ABI of liblre_b200 (include/lre_b200.h).  Argument checking and status
+// mapping only; the work is in lre_step1.cu / lre_step2.cu / lre_aux.cu /
+// lre_gen.cu.
+#include <atomic>
+#include <cstdio>
+#include <vector>
+
+#include "lre_internal.cuh"
+
+namespace lre {
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+int step1_impl(const void *counts, int dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end, void *ws,
+               size_t ws_bytes, void *out, int out_kind, int layout, cudaStream_t stream);
+size_t step1_workspace(int n, int64_t shots, int64_t w_begin, int64_t w_end);
+int step1_stage_impl(const void *counts, int dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end, void *ws,
+                     size_t ws_bytes, cudaStream_t stream);
+int step1_finish_impl(void *ws, size_t ws_bytes, int n, int64_t shots, void *out, int out_kind, int layout,
+                      cudaStream_t stream);
+int step1_num_passes(int n, int64_t shots);
+int64_t shard_quantum(int n, int64_t shots);
+int assemble_impl(const double *theta_mm, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s);
+int validate_impl(const void *counts, int dtype, int n, int64_t rows, int64_t shots, int64_t *result,
+                  cudaStream_t s);
+int finalize_impl(const int64_t *num, int n, int64_t shots, int layout, int64_t begin, int64_t end, double *theta,
+                  cudaStream_t s);
+int relayout_impl(const double *src, int src_layout, int n, double *dst, cudaStream_t s);
+int generate_impl(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, int exact, int64_t w_begin,
+                  int64_t w_end, void *out, int dtype, cudaStream_t s);
+}  // namespace lre
+
+static inline int64_t pow3_i(int n) {
+    int64_t r = 1;
+    for (int i = 0; i < n; ++i) r *= 3;
+    return r;
+}
+
+static inline int64_t dtype_max(int dtype) {
+    switch (dtype) {
+    case LRE_U8: return 255;
+    case LRE_U16: return 65535;
+    case LRE_I32: return 2147483647LL;
+    case LRE_I64: return INT64_MAX;
+    default: return -1;
+    }
+}
+
+static inline bool valid_n(int n) { return n >= 1 && n <= 16; }
+
+extern "C" {
+
+const char *lre_strerror(int status) {
+    switch (status) {
+    case LRE_OK: return "ok";
+    case LRE_EINVAL: return "invalid argument";
+    case LRE_ECUDA: return "CUDA error";
+    case LRE_ENOMEM: return "workspace too small";
+    case LRE_EUNSUPPORTED: return "unsupported size or dtype";
+    case LRE_EOVERFLOW: return "shots too large for the count dtype";
+    default: return "unknown status";
+    }
+}
+
+int lre_version(void) { return 100; }
+
+int64_t lre_launch_count(void) { return lre::g_launches.load(); }
+
+int64_t lre_shard_quantum(int n) { return valid_n(n) ? lre::shard_quantum(n, 1) : -1; }
+
+int lre_step1_workspace(int n, int64_t shots, int64_t w_begin, int64_t w_end, size_t *bytes) {
+    if (!valid_n(n) || !bytes || shots < 1) return LRE_EINVAL;
+    if (w_begin < 0 || w_end > pow3_i(n) || w_begin >= w_end) return LRE_EINVAL;
+    *bytes = lre::step1_workspace(n, shots, w_begin, w_end);
+    return LRE_OK;
+}
+
+int lre_step1(const void *counts, int count_dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end,
+              void *workspace, size_t workspace_bytes, void *out, int out_kind, int layout, lre_stream_t stream) {
+    if (!valid_n(n) || !counts || !out || shots < 1) return LRE_EINVAL;
+    if (dtype_max(count_dtype) < 0) return LRE_EINVAL;
+    if (shots > dtype_max(count_dtype) && count_dtype != LRE_I64) return LRE_EOVERFLOW;
+    if (w_begin < 0 || w_end > pow3_i(n) || w_begin >= w_end) return LRE_EINVAL;
+    if (out_kind != LRE_OUT_THETA_F64 && out_kind != LRE_OUT_NUM_I64) return LRE_EINVAL;
+    if (layout != LRE_LAYOUT_NATURAL && layout != LRE_LAYOUT_MASK_MAJOR) return LRE_EINVAL;
+    if (out_kind == LRE_OUT_THETA_F64 && (w_begin != 0 || w_end != pow3_i(n))) return LRE_EINVAL;
+    const int64_t q = lre::shard_quantum(n, shots);
+    if (w_begin % q || (w_end % q && w_end != pow3_i(n))) return LRE_EINVAL;
+    return lre::step1_impl(counts, count_dtype, n, shots, w_begin, w_end, workspace, workspace_bytes, out, out_kind,
+                           layout, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_step1_num_passes(int n, int64_t shots) {
+    if (!valid_n(n) || shots < 1) return -1;
+    return lre::step1_num_passes(n, shots);
+}
+
+int lre_step1_stage(const void *counts, int count_dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end,
+                    void *workspace, size_t workspace_bytes, lre_stream_t stream) {
+    if (!valid_n(n) || !counts || shots < 1) return LRE_EINVAL;
+    if (dtype_max(count_dtype) < 0) return LRE_EINVAL;
+    if (shots > dtype_max(count_dtype) && count_dtype != LRE_I64) return LRE_EOVERFLOW;
+    if (w_begin < 0 || w_end > pow3_i(n) || w_begin >= w_end) return LRE_EINVAL;
+    const int64_t q = lre::shard_quantum(n, shots);
+    if (w_begin % q || (w_end % q && w_end != pow3_i(n))) return LRE_EINVAL;
+    return lre::step1_stage_impl(counts, count_dtype, n, shots, w_begin, w_end, workspace, workspace_bytes,
+                                 reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_step1_finish(void *workspace, size_t workspace_bytes, int n, int64_t shots, void *out, int out_kind,
+                     int layout, lre_stream_t stream) {
+    if (!valid_n(n) || !out || shots < 1) return LRE_EINVAL;
+    if (out_kind != LRE_OUT_THETA_F64 && out_kind != LRE_OUT_NUM_I64) return LRE_EINVAL;
+    if (layout != LRE_LAYOUT_NATURAL && layout != LRE_LAYOUT_MASK_MAJOR) return LRE_EINVAL;
+    return lre::step1_finish_impl(workspace, workspace_bytes, n, shots, out, out_kind, layout,
+                                  reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_finalize(const int64_t *num, int n, int64_t shots, int layout, int64_t begin, int64_t end, double *theta,
+                 lre_stream_t stream) {
+    if (!valid_n(n) || shots < 1 || !num || !theta) return LRE_EINVAL;
+    if (begin < 0 || end > ((int64_t)1 << (2 * n))) return LRE_EINVAL;
+    return lre::finalize_impl(num, n, shots, layout, begin, end, theta, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_theta_relayout(const double *src, int src_layout, int n, double *dst, lre_stream_t stream) {
+    if (!valid_n(n) || !src || !dst || src == dst) return LRE_EINVAL;
+    if (src_layout != LRE_LAYOUT_NATURAL && src_layout != LRE_LAYOUT_MASK_MAJOR) return LRE_EINVAL;
+    return lre::relayout_impl(src, src_layout, n, dst, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_assemble(const double *theta_mm, int n, int64_t m_begin, int64_t m_end, double *mu_out, lre_stream_t stream) {
+    if (!valid_n(n) || !theta_mm || !mu_out) return LRE_EINVAL;
+    return lre::assemble_impl(theta_mm, n, m_begin, m_end, mu_out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_validate_counts(const void *counts, int count_dtype, int n, int64_t rows, int64_t shots, int64_t *result,
+                        lre_stream_t stream) {
+    if (!valid_n(n) || !counts || !result || rows < 1) return LRE_EINVAL;
+    return lre::validate_impl(counts, count_dtype, n, rows, shots, result, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_generate_counts(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, int exact, int64_t w_begin,
+                        int64_t w_end, void *out, int count_dtype, lre_stream_t stream) {
+    if (!valid_n(n) || !out) return LRE_EINVAL;
+    if (dtype_max(count_dtype) < 0) return LRE_EINVAL;
+    if (shots > dtype_max(count_dtype)) return LRE_EOVERFLOW;
+    if (w_begin < 0 || w_end > pow3_i(n) || w_begin > w_end) return LRE_EINVAL;
+    if (kind == LRE_STATE_PRODUCTZ && (bits < 0 || bits >= ((int64_t)1 << n))) return LRE_EINVAL;
+    return lre::generate_impl(kind, n, bits, shots, seed, exact, w_begin, w_end, out, count_dtype,
+                              reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+// Internal device helpers shared by the LRE kernels (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/lre_b200.h"
+
+namespace lre {
+
+// ---------------------------------------------------------------------------
+// compile-time helpers
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int pow3(int k) { return k <= 0 ? 1 : 3 * pow3(k - 1); }
+__host__ __device__ constexpr int popc_c(int x) { return x == 0 ? 0 : (x & 1) + popc_c(x >> 1); }
+
+// global launch counter (bench.py reports it as gpu_launches)
+void count_launch(int k = 1);
+
+// ---------------------------------------------------------------------------
+// count loads: 8 consecutive elements of the counts / intermediate tensor,
+// streamed with the evict-first (".cs") policy so they do not displace the
+// scattered output lines that L2 is merging.
+// ---------------------------------------------------------------------------
+template <typename A>
+__device__ __forceinline__ void load8(const uint8_t *p, A v[8]) {
+    uint2 u = __ldcs(reinterpret_cast<const uint2 *>(p));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = (A)((u.x >> (8 * i)) & 0xff);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[4 + i] = (A)((u.y >> (8 * i)) & 0xff);
+}
+template <typename A>
+__device__ __forceinline__ void load8(const uint16_t *p, A v[8]) {
+    uint4 u = __ldcs(reinterpret_cast<const uint4 *>(p));
+    v[0] = (A)(u.x & 0xffff); v[1] = (A)(u.x >> 16);
+    v[2] = (A)(u.y & 0xffff); v[3] = (A)(u.y >> 16);
+    v[4] = (A)(u.z & 0xffff); v[5] = (A)(u.z >> 16);
+    v[6] = (A)(u.w & 0xffff); v[7] = (A)(u.w >> 16);
+}
+template <typename A>
+__device__ __forceinline__ void load8(const int32_t *p, A v[8]) {
+    int4 a = __ldcs(reinterpret_cast<const int4 *>(p));
+    int4 b = __ldcs(reinterpret_cast<const int4 *>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+template <typename A>
+__device__ __forceinline__ void load8(const int64_t *p, A v[8]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        longlong2 q = __ldcs(reinterpret_cast<const longlong2 *>(p) + i);
+        v[2 * i] = (A)q.x;
+        v[2 * i + 1] = (A)q.y;
+    }
+}
+
+// scalar load used by the small (<8 column) tiles
+template <typename T> __device__ __forceinline__ int64_t load1(const T *p) { return (int64_t)__ldcs(p); }
+template <> __device__ __forceinline__ int64_t load1<uint8_t>(const uint8_t *p) { return (int64_t)*p; }
+template <> __device__ __forceinline__ int64_t load1<uint16_t>(const uint16_t *p) {
+    return (int64_t)__ldcs(reinterpret_cast<const unsigned short *>(p));
+}
+
+// ---------------------------------------------------------------------------
+// the per-qubit 6 -> 4 map A (SURVEY §0.1 "separable form"):
+//   rows (axis X,Y,Z) x outcome bit -> Pauli digit I,X,Y,Z
+//   I = sum of all six, X/Y/Z = (+1 outcome) - (-1 outcome) on that axis.
+// ---------------------------------------------------------------------------
+template <typename A>
+__device__ __forceinline__ void q6to4(A x0, A x1, A y0, A y1, A z0, A z1, A &I, A &X, A &Y, A &Z) {
+    I = (x0 + x1) + (y0 + y1) + (z0 + z1);
+    X = x0 - x1;
+    Y = y0 - y1;
+    Z = z0 - z1;
+}
+
+// Natural Pauli index i (base-4 digits, qubit 1 most significant) ->
+// mask-major index m * 2^n + a with m = X|Y bits and a = Y|Z bits
+// (SURVEY §0.1 "symplectic relabel"; reference pauli.py:262-289).
+__device__ __forceinline__ uint32_t compact_odd(uint64_t x) {
+    // take bits 1,3,5,... of x and pack them
+    x = (x >> 1) & 0x5555555555555555ull;
+    x = (x | (x >> 1)) & 0x3333333333333333ull;
+    x = (x | (x >> 2)) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | (x >> 4)) & 0x00ff00ff00ff00ffull;
+    x = (x | (x >> 8)) & 0x0000ffff0000ffffull;
+    x = (x | (x >> 16)) & 0x00000000ffffffffull;
+    return (uint32_t)x;
+}
+__device__ __forceinline__ uint32_t compact_even(uint64_t x) { return compact_odd(x << 1); }
+
+__device__ __forceinline__ void natural_to_ma(uint64_t i, uint32_t &m, uint32_t &a) {
+    uint32_t hi = compact_odd(i);   // digit >= 2  -> Y or Z
+    uint32_t lo = compact_even(i);  // digit odd   -> X or Z
+    a = hi;
+    m = hi ^ lo;                    // X (01) or Y (10)
+}
+
+__device__ __forceinline__ uint64_t spread_bits(uint32_t x) {
+    uint64_t v = x;
+    v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+    v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+    v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+    v = (v | (v << 2)) & 0x3333333333333333ull;
+    v = (v | (v << 1)) & 0x5555555555555555ull;
+    return v;
+}
+// (m, a) -> natural index: hi bit = a, lo bit = a ^ m
+__device__ __forceinline__ uint64_t ma_to_natural(uint32_t m, uint32_t a) {
+    return (spread_bits(a) << 1) | spread_bits(a ^ m);
+}
+
+// 3^k as an exact double (k <= 32)
+__device__ __forceinline__ double pow3d(int k) {
+    double g = 1.0;
+    for (int i = 0; i < k; ++i) g *= 3.0;
+    return g;
+}
+
+}  // namespace lre

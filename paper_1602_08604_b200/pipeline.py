@@ -1,0 +1,326 @@
+"""The LRE pipeline on B200 — drop-in for the reference's pipeline.py.
+
+Same entry points, argument meaning and error behaviour as the reference
+(``/root/reference/pkg/src/pauli_lre/pipeline.py``):
+
+* ``step_one_least_squares(record_or_source, workers=1, kernel=...)``
+  (pipeline.py:116-138) — counts -> theta, natural order, fp64;
+* ``step_two_assemble(theta, workers=1)`` (pipeline.py:141-161) — theta -> mu;
+* ``step_three_project(mu)`` (pipeline.py:187-208) — adjacent step (iii);
+* ``reconstruct(record_or_source, workers=1, kernel=...)`` (pipeline.py:224-249)
+  returning ``ReconstructionResult`` with the same ``timings`` keys.
+
+Steps (i) and (ii) run only on the sm_100a kernels of liblre_b200.so (there
+is no CPU path).  ``workers`` is accepted for signature compatibility (the
+GPU decides its own parallelism); ``kernel`` accepts the reference names
+"fast" and "paper-direct" (both map to the same B200 kernels, their outputs
+being identical by construction in the reference as well) and "b200".
+Sources: ``MeasurementRecord`` (host counts; copied to HBM, validated on the
+device), ``DeviceRecord`` (counts already in HBM) or ``StateDescriptor``
+(exact noiseless record generated on the device; the reference's
+ExactFrequencies).  Outputs are numpy arrays by default; pass
+``as_tensor=True`` to keep torch CUDA tensors.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, pauli
+from .records import DeviceRecord, MeasurementRecord, lre_dtype_of
+from .simulate import StateDescriptor, exact_record
+
+KERNELS = ("b200", "fast", "paper-direct")
+DENSE_PIPELINE_MAX_QUBITS = 14  # reference caps at 12 (pipeline.py:31); the B200 path lifts it
+
+_HERMITIAN_TOL = 1e-10  # pipeline.py:36
+_TRACE_TOL = 1e-8  # pipeline.py:37
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("the B200 LRE path needs a CUDA device; there is no CPU fallback")
+    return torch
+
+
+def _device(device):
+    torch = _torch()
+    return torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+
+
+def _check_kernel(kernel: str) -> None:
+    if kernel not in KERNELS:
+        raise ValueError(f"unknown kernel {kernel!r}, expected one of {KERNELS}")
+
+
+# ---------------------------------------------------------------------------
+# sources
+# ---------------------------------------------------------------------------
+
+def to_device_record(record_or_source, device=None, stream=None) -> DeviceRecord:
+    """Resolve any supported source into a validated DeviceRecord (pipeline.py:54-59)."""
+    torch = _torch()
+    dev = _device(device)
+    if isinstance(record_or_source, DeviceRecord):
+        return record_or_source.validate(stream)
+    if isinstance(record_or_source, StateDescriptor):
+        if not record_or_source.dyadic:
+            raise ValueError(
+                f"state {record_or_source.label()} has non-dyadic probabilities; the device path consumes "
+                "integer counts, sample a record with simulate.sample_counts instead"
+            )
+        return exact_record(record_or_source, device=dev).validate(stream)
+    if isinstance(record_or_source, MeasurementRecord):
+        rec = record_or_source
+        n = pauli.check_qubit_count(rec.n)
+        counts = np.asarray(rec.counts)
+        if tuple(counts.shape) != (3**n, 1 << n):
+            raise ValueError(f"counts shape {counts.shape} != {(3**n, 1 << n)} for n={n}")
+        if not np.issubdtype(counts.dtype, np.integer):
+            raise ValueError(f"counts must be integers, got dtype {counts.dtype}")
+        if counts.dtype not in (np.uint8, np.uint16, np.int32, np.int64):
+            counts = counts.astype(np.int64)
+        host = torch.from_numpy(np.ascontiguousarray(counts))
+        dcounts = host.to(dev, non_blocking=False)
+        drec = DeviceRecord(n=n, shots=int(rec.shots), counts=dcounts, seed=rec.seed, state=rec.state)
+        drec.validate(stream)
+        rec._validated = True
+        return drec
+    raise TypeError(
+        f"unsupported source {type(record_or_source).__name__}: pass a MeasurementRecord, DeviceRecord "
+        "or StateDescriptor"
+    )
+
+
+# ---------------------------------------------------------------------------
+# device plan: buffers + launches for one (n, shots, dtype) shape
+# ---------------------------------------------------------------------------
+
+class LREPlan:
+    """Preallocated HBM buffers and the launch sequence of one reconstruction.
+
+    step1: counts -> theta (MASK_MAJOR fp64), 1-3 fold-pass launches;
+    step2: theta -> mu (row-major complex128), 1 launch.
+    """
+
+    def __init__(self, n: int, shots: int, device=None, with_mu: bool = True):
+        torch = _torch()
+        self.n = pauli.check_qubit_count(n)
+        self.shots = int(shots)
+        self.device = _device(device)
+        import ctypes
+
+        L = _lib.load()
+        ws = ctypes.c_size_t(0)
+        _lib.check(L.lre_step1_workspace(self.n, self.shots, 0, 3**self.n, ctypes.byref(ws)), "lre_step1_workspace")
+        self.ws_bytes = int(ws.value)
+        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=self.device)
+        self.theta_mm = torch.empty(4**self.n, dtype=torch.float64, device=self.device)
+        d = 1 << self.n
+        self.mu = torch.empty((d, d), dtype=torch.complex128, device=self.device) if with_mu else None
+        self.passes = int(L.lre_step1_num_passes(self.n, self.shots))
+
+    def step1(self, counts, count_dtype: int, stream) -> None:
+        _lib.call("lre_step1", counts.data_ptr(), count_dtype, self.n, self.shots, 0, 3**self.n,
+                  self.ws.data_ptr(), self.ws_bytes, self.theta_mm.data_ptr(), _lib.OUT_THETA_F64,
+                  _lib.MASK_MAJOR, stream.cuda_stream)
+
+    def stage(self, chunk, count_dtype: int, w_begin: int, w_end: int, stream) -> None:
+        _lib.call("lre_step1_stage", chunk.data_ptr(), count_dtype, self.n, self.shots, int(w_begin), int(w_end),
+                  self.ws.data_ptr(), self.ws_bytes, stream.cuda_stream)
+
+    def finish(self, stream) -> None:
+        _lib.call("lre_step1_finish", self.ws.data_ptr(), self.ws_bytes, self.n, self.shots,
+                  self.theta_mm.data_ptr(), _lib.OUT_THETA_F64, _lib.MASK_MAJOR, stream.cuda_stream)
+
+    def step2(self, stream) -> None:
+        d = 1 << self.n
+        _lib.call("lre_assemble", self.theta_mm.data_ptr(), self.n, 0, d, self.mu.data_ptr(), stream.cuda_stream)
+
+    def run(self, counts, count_dtype: int, stream) -> None:
+        self.step1(counts, count_dtype, stream)
+        self.step2(stream)
+
+    def theta_natural(self, stream, out=None):
+        torch = _torch()
+        out = torch.empty_like(self.theta_mm) if out is None else out
+        _lib.call("lre_theta_relayout", self.theta_mm.data_ptr(), _lib.MASK_MAJOR, self.n, out.data_ptr(),
+                  stream.cuda_stream)
+        return out
+
+
+def _theta_mm_from(theta, n, device, stream):
+    """natural-order theta (numpy or tensor) -> mask-major device tensor."""
+    torch = _torch()
+    t = theta if isinstance(theta, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(theta, dtype=np.float64))
+    t = t.to(device=device, dtype=torch.float64).contiguous()
+    mm = torch.empty_like(t)
+    _lib.call("lre_theta_relayout", t.data_ptr(), _lib.NATURAL, n, mm.data_ptr(), stream.cuda_stream)
+    return mm
+
+
+# ---------------------------------------------------------------------------
+# reference entry points
+# ---------------------------------------------------------------------------
+
+def step_one_least_squares(record_or_source, workers: int = 1, kernel: str = "b200", *, device=None,
+                           as_tensor: bool = False):
+    """Least-squares Pauli coefficients theta (natural order), pipeline.py:116-138."""
+    _check_kernel(kernel)
+    torch = _torch()
+    rec = to_device_record(record_or_source, device)
+    n = pauli.check_qubit_count(rec.n)
+    stream = torch.cuda.current_stream(rec.counts.device)
+    theta = torch.empty(4**n, dtype=torch.float64, device=rec.counts.device)
+    if rec.w_begin != 0 or rec.w_end != 3**n:
+        raise ValueError("step_one_least_squares needs the full setting range")
+    import ctypes
+
+    ws = ctypes.c_size_t(0)
+    _lib.check(_lib.load().lre_step1_workspace(n, int(rec.shots), 0, 3**n, ctypes.byref(ws)), "lre_step1_workspace")
+    buf = torch.empty(max(int(ws.value), 256), dtype=torch.uint8, device=rec.counts.device)
+    _lib.call("lre_step1", rec.counts.data_ptr(), rec.lre_dtype, n, int(rec.shots), 0, 3**n, buf.data_ptr(),
+              int(ws.value), theta.data_ptr(), _lib.OUT_THETA_F64, _lib.NATURAL, stream.cuda_stream)
+    return theta if as_tensor else theta.cpu().numpy()
+
+
+def step_two_assemble(theta, workers: int = 1, *, device=None, as_tensor: bool = False):
+    """Dense Hermitian estimate mu from theta (natural order), pipeline.py:141-161."""
+    torch = _torch()
+    size = int(theta.shape[0])
+    n = (size.bit_length() - 1) // 2
+    if len(theta.shape) != 1 or size != 4**n:
+        raise ValueError(f"theta length {tuple(theta.shape)} is not 4**n")
+    pauli.check_qubit_count(n)
+    if n > DENSE_PIPELINE_MAX_QUBITS:
+        raise NotImplementedError(f"dense assembly is built for n <= {DENSE_PIPELINE_MAX_QUBITS}")
+    dev = theta.device if isinstance(theta, torch.Tensor) and theta.is_cuda else _device(device)
+    stream = torch.cuda.current_stream(dev)
+    mm = _theta_mm_from(theta, n, dev, stream)
+    d = 1 << n
+    mu = torch.empty((d, d), dtype=torch.complex128, device=dev)
+    _lib.call("lre_assemble", mm.data_ptr(), n, 0, d, mu.data_ptr(), stream.cuda_stream)
+    return mu if as_tensor else mu.cpu().numpy()
+
+
+def project_spectrum_to_simplex(values):
+    """Scan-from-smallest simplex projection (pipeline.py:164-184), on the device."""
+    torch = _torch()
+    is_np = not isinstance(values, torch.Tensor)
+    v = torch.as_tensor(np.asarray(values, dtype=np.float64) if is_np else values, dtype=torch.float64)
+    v = v.to(_device(None) if not v.is_cuda else v.device)
+    u, order = torch.sort(v)
+    k = u.shape[0]
+    prefix = torch.cat([torch.zeros(1, dtype=u.dtype, device=u.device), torch.cumsum(u[:-1], 0)])
+    remaining = k - torch.arange(k, device=u.device, dtype=u.dtype)
+    crossing = (u + prefix / remaining) >= 0.0
+    stop = int(torch.argmax(crossing.to(torch.int8)).item())
+    out = torch.zeros_like(u)
+    out[stop:] = u[stop:] + prefix[stop] / (k - stop)
+    res = torch.empty_like(out)
+    res[order] = out
+    return res.cpu().numpy() if is_np else res
+
+
+def step_three_project(mu):
+    """Closest physical state (pipeline.py:187-208); adjacent to the hot path.
+
+    Uses the device Hermitian eigensolver (cuSOLVER via torch.linalg.eigh)
+    and returns ``(rho, eigenvalues ascending)``; an already-PSD ``mu`` is
+    returned unchanged (the same object), as in the reference.
+    """
+    torch = _torch()
+    is_np = not isinstance(mu, torch.Tensor)
+    m = torch.from_numpy(np.asarray(mu)) if is_np else mu
+    m = m.to(device=_device(None) if not m.is_cuda else m.device, dtype=torch.complex128)
+    d = m.shape[0]
+    if m.dim() != 2 or m.shape[1] != d:
+        raise ValueError(f"expected a square matrix, got shape {tuple(m.shape)}")
+    asym = float((m - m.conj().T).abs().max().item())
+    if asym > _HERMITIAN_TOL:
+        raise ValueError(f"matrix is not Hermitian (max asymmetry {asym:.3e})")
+    trace = float(torch.diagonal(m).real.sum().item())
+    if abs(trace - 1.0) > _TRACE_TOL:
+        raise ValueError(f"trace {trace!r} deviates from 1 beyond {_TRACE_TOL}")
+    evals, evecs = torch.linalg.eigh(m)
+    if float(evals[0].item()) >= 0.0:
+        return (mu, evals.cpu().numpy()) if is_np else (mu, evals)
+    lam = project_spectrum_to_simplex(evals)
+    rho = (evecs * lam.to(evecs.dtype)) @ evecs.conj().T
+    return (rho.cpu().numpy(), lam.cpu().numpy()) if is_np else (rho, lam)
+
+
+@dataclass
+class ReconstructionResult:
+    """pipeline.py:211-221."""
+
+    theta: object
+    mu: object
+    rho: object
+    eigenvalues: object  # spectrum of rho, ascending
+    timings: dict
+
+    @property
+    def n(self) -> int:
+        return (int(self.theta.shape[0]).bit_length() - 1) // 2
+
+
+def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, device=None, project: bool = True,
+                as_tensor: bool = False) -> ReconstructionResult:
+    """All three steps with per-step device timings (pipeline.py:224-249).
+
+    Validation happens before the timer, as in the reference.  ``timings``
+    has the reference keys t_step1_s / t_step2_s / t_step3_s / t_total_s /
+    threads / kernel, measured with CUDA events, plus gpus and
+    t_theta_export_s (natural-order theta export, outside the hot path).
+    """
+    _check_kernel(kernel)
+    torch = _torch()
+    rec = to_device_record(record_or_source, device)
+    n = pauli.check_qubit_count(rec.n)
+    if n > DENSE_PIPELINE_MAX_QUBITS:
+        raise ValueError(
+            f"n={n} needs a dense {2**n}x{2**n} complex allocation "
+            f"({(4**n * 16) >> 20} MB); the dense pipeline is capped at n={DENSE_PIPELINE_MAX_QUBITS}"
+        )
+    dev = rec.counts.device
+    stream = torch.cuda.current_stream(dev)
+    plan = LREPlan(n, rec.shots, dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev[0].record(stream)
+    plan.step1(rec.counts, rec.lre_dtype, stream)
+    ev[1].record(stream)
+    plan.step2(stream)
+    ev[2].record(stream)
+    if project:
+        rho, evals = step_three_project(plan.mu)
+    else:
+        rho, evals = plan.mu, None
+    ev[3].record(stream)
+    theta = plan.theta_natural(stream)
+    ev[4].record(stream)
+    ev[4].synchronize()
+    t1 = ev[0].elapsed_time(ev[1]) / 1e3
+    t2 = ev[1].elapsed_time(ev[2]) / 1e3
+    t3 = ev[2].elapsed_time(ev[3]) / 1e3
+    timings = {
+        "t_step1_s": t1,
+        "t_step2_s": t2,
+        "t_step3_s": t3,
+        "t_total_s": t1 + t2 + t3,
+        "threads": workers,
+        "kernel": kernel,
+        "gpus": 1,
+        "t_theta_export_s": ev[3].elapsed_time(ev[4]) / 1e3,
+    }
+    mu = plan.mu
+    if not as_tensor:
+        same = rho is mu
+        theta, mu = theta.cpu().numpy(), mu.cpu().numpy()
+        rho = mu if same else rho.cpu().numpy()
+        evals = None if evals is None else evals.cpu().numpy()
+    return ReconstructionResult(theta=theta, mu=mu, rho=rho, eigenvalues=evals, timings=timings)

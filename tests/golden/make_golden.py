@@ -1,0 +1,200 @@
+"""Generate the golden parity fixtures from the REAL reference package.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``pauli_lre`` from ``/root/reference/pkg/src`` (numba cache
+redirected to /tmp so nothing is written into the read-only tree), runs the
+reference's own step (i)/(ii)/(iii) on seeded inputs and writes the inputs and
+outputs under ``tests/golden/``.  The GPU box never reads /root/reference: the
+tests there only read these committed fixtures.
+
+Cases:
+  kat.npz          SPEC known-answer tests KAT1/2/4/5/8
+  blocks_n3.npz    index-map building blocks (pauli.py:153-297) at n=3
+  c1_*.npz         n=4 GHZ exact (shots 16) and sampled (1000 shots, seed 1602)
+  small_*.npz      n=1..6 random/productz/maxmixed records (KAT10-style)
+  c2_w8.npz        n=8 W state, 1000 shots, seed 1602 (counts stored as uint16)
+  c3_random10.npz  n=10 Ginibre state (_random_density(10, 8604)), 1000 shots,
+                   seed 1602 — counts are NOT stored (120 MB); the fixture
+                   holds their sha256 and strided samples of theta/mu; the
+                   tests regenerate the counts with the oracle's restatement
+                   of simulate.sample_counts and check the hash first.
+  validate.npz     MeasurementRecord.validate error messages.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF = "/root/reference/pkg/src"
+
+os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "numba_golden"))
+sys.path.insert(0, REF)
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from pauli_lre import pauli, pipeline, simulate  # noqa: E402  (the reference)
+from pauli_lre.records import MeasurementRecord  # noqa: E402
+
+from oracle import lre_oracle as O  # noqa: E402
+
+SEED = 1602
+
+
+def _save(name, **arrays):
+    path = os.path.join(HERE, name)
+    np.savez_compressed(path, **arrays)
+    print(f"wrote {name} ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+def _run_reference(counts, n, shots, with_step3=True):
+    rec = MeasurementRecord(n=n, shots=shots, counts=np.asarray(counts, dtype=np.int64))
+    theta = pipeline.step_one_least_squares(rec, workers=1)
+    mu = pipeline.step_two_assemble(theta, workers=1)
+    out = dict(counts=np.asarray(counts), n=n, shots=shots, theta=theta, mu=mu)
+    if with_step3:
+        rho, ev = pipeline.step_three_project(mu)
+        out.update(rho=rho, eigenvalues=ev)
+    return out
+
+
+def _reference_sample_from_rho(rho, n, shots, seed):
+    """Reference primitives: dense_to_theta (complex) -> _theta_probability_block
+    -> _setting_rng(seed, w).multinomial (simulate.py:114-151, 216-242)."""
+    theta = simulate.dense_to_theta(np.asarray(rho, dtype=np.complex128))
+    settings = 3**n
+    counts = np.empty((settings, 1 << n), dtype=np.int64)
+    block = max(1, (1 << 18) >> n)
+    for start in range(0, settings, block):
+        stop = min(settings, start + block)
+        probs = np.clip(simulate._theta_probability_block(theta, start, stop, n), 0.0, 1.0)
+        for row, w in enumerate(range(start, stop)):
+            p = np.clip(probs[row], 0.0, None)
+            counts[w] = simulate._setting_rng(seed, w).multinomial(shots, p / p.sum())
+    return counts
+
+
+def kat():
+    sq2 = 1.0 / np.sqrt(2.0)
+    kat1_counts = np.array([[1, 1], [1, 1], [2, 0]], dtype=np.int64)
+    kat2_counts = np.array([[1, 1], [1, 1], [1, 1]], dtype=np.int64)
+    t1 = pipeline.step_one_least_squares(MeasurementRecord(1, 2, kat1_counts))
+    t2 = pipeline.step_one_least_squares(MeasurementRecord(1, 2, kat2_counts))
+    assert np.allclose(t1, [sq2, 0, 0, sq2]) and np.allclose(t2, [sq2, 0, 0, 0])
+    mu4 = pipeline.step_two_assemble(np.array([sq2, 0, 0, sq2]))
+    mu5 = pipeline.step_two_assemble(np.array([sq2, 0, 0, 0]))
+    p8a = pipeline.project_spectrum_to_simplex(np.array([1.02, 0.04, -0.03, -0.03]))
+    p8b = pipeline.project_spectrum_to_simplex(np.array([0.6, 0.5, -0.1]))
+    _save("kat.npz", kat1_counts=kat1_counts, kat1_theta=t1, kat2_counts=kat2_counts, kat2_theta=t2,
+          kat4_mu=mu4, kat5_mu=mu5, kat8a=p8a, kat8b=p8b)
+
+
+def blocks():
+    n = 3
+    locs = pauli.nonzero_locations_block(pauli.setting_digit_rows(0, 3**n, n), n)
+    gather = np.stack([pauli.omega_gather_indices(m, n) for m in range(1 << n)])
+    phase = np.stack([pauli.omega_phase_factors(m, n) for m in range(1 << n)])
+    wht_in = np.random.default_rng(5).standard_normal((4, 64))
+    _save("blocks_n3.npz", locs=locs, gather=gather, phase=phase, xtx=pauli.xtx_diagonal_full(n),
+          wht_in=wht_in, wht_out=pauli.walsh_hadamard_transform(wht_in),
+          digit_rows=pauli.setting_digit_rows(0, 3**n, n))
+
+
+def c1():
+    ghz = simulate.StateDescriptor("ghz", 4)
+    rec = simulate.exact_record(ghz)
+    _save("c1_ghz4_exact.npz", **_run_reference(rec.counts, 4, rec.shots))
+    rec = simulate.sample_counts(ghz, shots=1000, seed=SEED)
+    _save("c1_ghz4_sampled.npz", **_run_reference(rec.counts, 4, 1000))
+
+
+def small():
+    cases = [
+        ("small_random1.npz", simulate.StateDescriptor("random", 1, state_seed=3), 100, 11),
+        ("small_random2.npz", simulate.StateDescriptor("random", 2, state_seed=4), 500, 12),
+        ("small_random3.npz", simulate.StateDescriptor("random", 3, state_seed=5), 4096, 13),
+        ("small_productz5.npz", simulate.StateDescriptor("productz", 5, bits=0b10110), None, None),
+        ("small_maxmixed6.npz", simulate.StateDescriptor("maxmixed", 6), None, None),
+        ("small_ghz2_sampled.npz", simulate.StateDescriptor("ghz", 2), 1000, 7),
+    ]
+    for name, state, shots, seed in cases:
+        if shots is None:
+            rec = simulate.exact_record(state)
+        else:
+            rec = simulate.sample_counts(state, shots=shots, seed=seed)
+        _save(name, **_run_reference(rec.counts, state.n, rec.shots))
+
+
+def c2():
+    n = 8
+    rho = O.dense_state("w", n)
+    counts = _reference_sample_from_rho(rho, n, 1000, SEED)
+    ours = O.sample_counts_from_theta(O.dense_to_theta(rho), n, 1000, SEED)
+    assert np.array_equal(ours, counts), "oracle generator diverges from reference primitives at n=8"
+    out = _run_reference(counts, n, 1000, with_step3=False)
+    out["counts"] = counts.astype(np.uint16)
+    _save("c2_w8.npz", **out)
+
+
+def c3():
+    n = 10
+    rho = simulate._random_density(n, 8604)
+    counts = _reference_sample_from_rho(rho, n, 1000, SEED)
+    ours = O.sample_counts_from_theta(O.dense_to_theta(O.dense_state("random", n, seed=8604)), n, 1000, SEED)
+    assert np.array_equal(ours, counts), "oracle generator diverges from reference primitives at n=10"
+    rec = MeasurementRecord(n=n, shots=1000, counts=counts)
+    theta = pipeline.step_one_least_squares(rec, workers=8)
+    mu = pipeline.step_two_assemble(theta, workers=1)
+    stride_t, stride_m = 97, 13
+    _save("c3_random10.npz", n=n, shots=1000, seed=SEED, state_seed=8604,
+          counts_sha256=np.array(hashlib.sha256(counts.astype(np.int64).tobytes()).hexdigest()),
+          theta_stride=stride_t, theta_sample=theta[::stride_t], theta_norm=np.linalg.norm(theta),
+          mu_stride=stride_m, mu_sample=mu.ravel()[::stride_m], mu_norm=np.linalg.norm(mu),
+          mu_diag=np.diag(mu).copy())
+
+
+def validate_messages():
+    msgs = {}
+    rng = np.random.default_rng(20240811)
+    counts = rng.multinomial(50, np.full(4, 0.25), size=9).astype(np.int64)
+    counts[3, 0] += 1
+    try:
+        MeasurementRecord(n=2, shots=50, counts=counts).validate()
+    except ValueError as exc:
+        msgs["bad_row_sum"] = str(exc)
+    bad = counts.copy()
+    bad[3, 0] -= 1
+    bad[5, 1] = -1
+    try:
+        MeasurementRecord(n=2, shots=50, counts=bad).validate()
+    except ValueError as exc:
+        msgs["negative"] = str(exc)
+    try:
+        MeasurementRecord(n=2, shots=50, counts=counts[:8]).validate()
+    except ValueError as exc:
+        msgs["shape"] = str(exc)
+    try:
+        MeasurementRecord(n=2, shots=50, counts=counts.astype(float)).validate()
+    except ValueError as exc:
+        msgs["dtype"] = str(exc)
+    ok = counts.copy()
+    ok[3, 0] -= 1
+    _save("validate.npz", counts_bad_row=counts, counts_ok=ok, messages=np.array(json.dumps(msgs)))
+
+
+if __name__ == "__main__":
+    kat()
+    blocks()
+    c1()
+    small()
+    validate_messages()
+    c2()
+    c3()
