@@ -81,7 +81,7 @@ int lre_step1(const void *counts, int count_dtype, int n, int64_t shots, int64_t
               int64_t w_end, void *workspace, size_t workspace_bytes, void *out, int out_kind,
               int layout, lre_stream_t stream);
 
-/* Alignment quantum of setting shards for lre_step1 (3^q1 of the first pass). */
+/* Alignment quantum of setting shards for lre_step1: 3^min(n, 7) (a multiple of every first-pass tile). */
 int64_t lre_shard_quantum(int n);
 
 /* Number of fold passes step (i) runs at this size (1 for n <= 7). */
@@ -112,15 +112,18 @@ int lre_finalize(const int64_t *num, int n, int64_t shots, int layout, int64_t b
 int lre_theta_relayout(const double *src, int src_layout, int n, double *dst, lre_stream_t stream);
 
 /*
- * Step (ii): theta (device, MASK_MAJOR slice holding masks [m_begin, m_end):
- * theta_mm[(m - m_begin)*2^n + a]) -> mu (device, complex128
- * as interleaved doubles).  S = m_end - m_begin must be a power of two and
- * m_begin a multiple of S; mu is written as d rows x S columns:
+ * Step (ii): theta (device) -> mu (device, complex128 as interleaved
+ * doubles) for the X/Y masks [m_begin, m_end).
+ *   layout == LRE_LAYOUT_NATURAL:     theta is the full natural-order vector;
+ *   layout == LRE_LAYOUT_MASK_MAJOR:  theta is the slice of those masks,
+ *                                     theta[(m - m_begin)*2^n + a].
+ * S = m_end - m_begin must be a power of two and m_begin a multiple of S; mu
+ * is written as d rows x S columns:
  *   mu_out[r*S + c] = mu[r, ((r / S) ^ (m_begin / S)) * S + c]
  * (S = 2^n gives the full row-major matrix).  Replaces reference
  * pipeline.py:141-161 (step_two_assemble) and pauli.py:270-297.
  */
-int lre_assemble(const double *theta_mm, int n, int64_t m_begin, int64_t m_end, double *mu_out,
+int lre_assemble(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu_out,
                  lre_stream_t stream);
 
 /*

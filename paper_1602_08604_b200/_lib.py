@@ -33,7 +33,7 @@ _SIGNATURES = {
     "lre_step1_finish": (_i, [_vp, _sz, _i, _i64, _vp, _i, _i, _vp]),
     "lre_finalize": (_i, [_vp, _i, _i64, _i, _i64, _i64, _vp, _vp]),
     "lre_theta_relayout": (_i, [_vp, _i, _i, _vp, _vp]),
-    "lre_assemble": (_i, [_vp, _i, _i64, _i64, _vp, _vp]),
+    "lre_assemble": (_i, [_vp, _i, _i, _i64, _i64, _vp, _vp]),
     "lre_validate_counts": (_i, [_vp, _i, _i, _i64, _i64, _vp, _vp]),
     "lre_generate_counts": (_i, [_i, _i, _i64, _i64, _u64, _i, _i64, _i64, _vp, _i, _vp]),
 }

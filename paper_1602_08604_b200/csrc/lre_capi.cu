@@ -20,7 +20,7 @@ int step1_finish_impl(void *ws, size_t ws_bytes, int n, int64_t shots, void *out
                       cudaStream_t stream);
 int step1_num_passes(int n, int64_t shots);
 int64_t shard_quantum(int n, int64_t shots);
-int assemble_impl(const double *theta_mm, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s);
+int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s);
 int validate_impl(const void *counts, int dtype, int n, int64_t rows, int64_t shots, int64_t *result,
                   cudaStream_t s);
 int finalize_impl(const int64_t *num, int n, int64_t shots, int layout, int64_t begin, int64_t end, double *theta,
@@ -62,7 +62,7 @@ const char *lre_strerror(int status) {
     }
 }
 
-int lre_version(void) { return 100; }
+int lre_version(void) { return 200; }
 
 int64_t lre_launch_count(void) { return lre::g_launches.load(); }
 
@@ -129,9 +129,11 @@ int lre_theta_relayout(const double *src, int src_layout, int n, double *dst, lr
     return lre::relayout_impl(src, src_layout, n, dst, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int lre_assemble(const double *theta_mm, int n, int64_t m_begin, int64_t m_end, double *mu_out, lre_stream_t stream) {
-    if (!valid_n(n) || !theta_mm || !mu_out) return LRE_EINVAL;
-    return lre::assemble_impl(theta_mm, n, m_begin, m_end, mu_out, reinterpret_cast<cudaStream_t>(stream));
+int lre_assemble(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu_out,
+                 lre_stream_t stream) {
+    if (!valid_n(n) || !theta || !mu_out) return LRE_EINVAL;
+    if (layout != LRE_LAYOUT_NATURAL && layout != LRE_LAYOUT_MASK_MAJOR) return LRE_EINVAL;
+    return lre::assemble_impl(theta, layout, n, m_begin, m_end, mu_out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int lre_validate_counts(const void *counts, int count_dtype, int n, int64_t rows, int64_t shots, int64_t *result,

@@ -1,31 +1,30 @@
 // Step (i) of the LRE hot path on B200: counts (3^n x 2^n) -> theta (4^n).
 //
 // Reference: pipeline.py:116-138 (step_one_least_squares), _kernels.py:34-56
-// (accumulate_fast: per-setting WHT + scatter) and pauli.py:153-209 (support
+// (accumulate_fast: per-setting WHT + scatter), pauli.py:153-209 (support
 // locations, Gram diagonal).
 //
-// B200 design: step (i) is the tensor map A^{(x)n} on the
-// 6^n count tensor, A = the per-qubit 6->4 map (rows X,Y,Z x outcome bit ->
-// Pauli digit).  It is evaluated in "fold passes"; a pass consumes the Q
-// lowest-stride qubits of its input
-//     X[P][3^h][3^Q][2^h][2^Q]  (row-major)
-// and writes
-//     Y[4^Q][P][3^h][2^h]
-// so the next pass again finds its qubits at the lowest strides, and after
-// the last pass Y is theta in natural order.  One CTA owns one tile
-// (3^Q rows x 2^Q contiguous columns; TPC tiles for small Q) and keeps all
-// 4^Q partial sums on chip while streaming the tile from HBM once:
-//   Phase A   each thread reduces 3 qubits fully in registers
-//             (27 rows x 8 contiguous columns -> 64 values, int32, exact);
-//   Phase A2  Walsh-Hadamard butterfly over the tile's column-group bits in
-//             shared memory;
-//   Phase B   each warp folds the staged row-block digits for one butterfly
-//             index t and emits final values (or accumulates the phase digit
-//             in shared memory).
-// All arithmetic is exact integer arithmetic; the only rounding is the final
-// fp64 epilogue theta = N / shots * 2^{-n/2} / 3^{zc}.
+// Step (i) is the tensor map A^{(x)n} applied to the 6^n count tensor
+// (SURVEY §0.1 "separable form"): per qubit, the setting digit (X/Y/Z) and
+// the outcome bit (+1/-1) of that qubit map to one Pauli digit I/X/Y/Z.
+// The map is evaluated in passes, each consuming the lowest-stride qubits of
+// its input:
+//
+//   pass 1  (tile_pass_kernel)  counts -> Y1[aH][c][4^Q1]   Q1 = 6 or 7
+//           one tile = 3^Q1 rows x 2^Q1 contiguous columns; its 4^Q1 exact
+//           int32 outputs are written contiguously ("tile-major"), so every
+//           store is a coalesced 128-byte line.
+//   pass k  (vfold_kernel)      X[a][col][V] -> Y[A][B][4^Q][V]   Q <= 3
+//           lanes own consecutive elements of the contiguous V axis (the
+//           Pauli digits already produced), each thread transforms Q more
+//           qubits in registers; reads and writes are 128-byte lines.
+//
+// All arithmetic is exact integer arithmetic (int16x2 packed, int32, int64);
+// the only rounding is the final fp64 epilogue theta = N / shots * 2^{-n/2} /
+// 3^{zc} (pipeline.py:138, records.py:64).
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <vector>
 
 #include "lre_internal.cuh"
@@ -34,656 +33,765 @@ namespace lre {
 
 __constant__ double c_pow3[33];
 
-struct PassGeom {
-    int64_t P;       // finished-digit groups (4^{qubits done})
-    int64_t C;       // column blocks (2^h)
-    int64_t alo;     // valid input a-range [alo, ahi) within 3^{h+Q}
-    int64_t ahi;
-    int64_t aloH;    // a_H range of the tiles this launch computes
-    int64_t nH;      // number of a_H values computed
-    int64_t aHout0;  // a_H of the first row group held by the output buffer
-    int64_t nHout;   // number of a_H row groups held by the output buffer
-    int64_t RCout;   // P * nHout * C : stride between output slots
-    int64_t ntiles;  // P * nH * C
-    int64_t rowlen;  // C * 2^Q elements
-    int Q;
-    int final_pass;
-    int out_kind;    // LRE_OUT_*
-    int layout;      // LRE_LAYOUT_*
+// ===========================================================================
+// epilogue shared by both kernels
+// ===========================================================================
+enum { OUT_INTER = 0, OUT_THETA = 1, OUT_NUM = 2 };
+
+struct Final {
+    void *out;
+    int kind;    // OUT_INTER / OUT_THETA / OUT_NUM
+    int layout;  // LRE_LAYOUT_* (final outputs only)
     int n;
     int64_t shots;
-    double scale;    // 2^{-n/2}
+    double scale;  // 2^{-n/2}
 };
 
-// ---------------------------------------------------------------------------
-// epilogue: intermediate store or finished theta / numerators
-// ---------------------------------------------------------------------------
-// output position of tile t inside one output slot
-__device__ __forceinline__ int64_t tile_out_base(const PassGeom &g, int64_t t) {
-    const int64_t c = t % g.C;
-    const int64_t rest = t / g.C;
-    const int64_t aH = g.aloH + rest % g.nH;
-    const int64_t p = rest / g.nH;
-    return (p * g.nHout + (aH - g.aHout0)) * g.C + c;
-}
-
-template <typename Ta>
-__device__ __forceinline__ void emit(void *__restrict__ out, const PassGeom &g, int64_t slot, int64_t ob, Ta v) {
-    const int64_t idx = slot * g.RCout + ob;
-    if (!g.final_pass) {
-        reinterpret_cast<Ta *>(out)[idx] = v;
-        return;
-    }
+// store a finished numerator at natural Pauli index `nat`
+__device__ __forceinline__ void store_final(const Final &f, uint64_t nat, int64_t v) {
     uint32_t m, a;
-    natural_to_ma((uint64_t)idx, m, a);
-    const uint64_t pos = g.layout == LRE_LAYOUT_MASK_MAJOR ? (((uint64_t)m << g.n) | a) : (uint64_t)idx;
-    if (g.out_kind == LRE_OUT_NUM_I64) {
-        reinterpret_cast<int64_t *>(out)[pos] = (int64_t)v;
+    natural_to_ma(nat, m, a);
+    const uint64_t pos = f.layout == LRE_LAYOUT_MASK_MAJOR ? (((uint64_t)m << f.n) | a) : nat;
+    if (f.kind == OUT_NUM) {
+        reinterpret_cast<int64_t *>(f.out)[pos] = v;
     } else {
-        const int zc = g.n - __popc(m | a);
-        reinterpret_cast<double *>(out)[pos] = ((double)v / (double)g.shots) * g.scale / c_pow3[zc];
+        const int zc = f.n - __popc(m | a);
+        reinterpret_cast<double *>(f.out)[pos] = ((double)v / (double)f.shots) * f.scale / c_pow3[zc];
     }
 }
 
-// ---------------------------------------------------------------------------
-// in-thread transform of 3 qubits: 27 rows x 8 contiguous columns -> 64
-// values indexed d = d1*16 + d2*4 + d3 (local qubit order, first = slowest
-// row digit = most significant column bit).  `sink(off, v[16])` receives the
-// 16 values with first digit d1 = off/16 as soon as they are final.
-// ---------------------------------------------------------------------------
-template <typename Tin, typename Ts, typename RowPtr, typename Sink>
-__device__ __forceinline__ void transform3(RowPtr rowptr, int64_t col0, Sink sink) {
-    Ts accI[16];
+// ===========================================================================
+// pass 1: tile kernel
+// ===========================================================================
+// A tile of Q = 6 qubits is processed in two levels of three qubits:
+//   L1 (warps 0-6): item (rb, g) = 27 consecutive rows x 8 contiguous
+//       columns; three qubits reduced in registers -> 64 values, staged.
+//   L2 (warps 7-8): one thread per staged value index `dlo`: the 27 x 8
+//       staged values of the tile -> three more qubits -> 64 values per
+//       thread, written as coalesced lines.
+// L1 of sub-tile s overlaps L2 of sub-tile s-1 (double-buffered staging, one
+// __syncthreads per sub-tile).  A Q = 7 tile is six Q = 6 sub-tiles (its top
+// setting digit r1 x top outcome bit b1) combined by the L2 threads.
+//
+// SMALL mode (shots <= 1213): L1 keeps two outcomes per 32-bit word
+// (w = lo + 65536*hi, exact mod 2^32) so each add works on two counts; the
+// staged values fit int16 (|v| <= 27*shots).
+constexpr int P1_L1_WARPS = 7;
+constexpr int P1_L2_WARPS = 2;
+constexpr int P1_THREADS = 32 * (P1_L1_WARPS + P1_L2_WARPS);
+constexpr int P1_ITEMS = 216;
+constexpr int SMALL_MAX_SHOTS = 1213;  // 27 * shots <= 32767
+
+template <bool SMALL> struct Stage {
+    using T = typename std::conditional<SMALL, int16_t, int32_t>::type;
+    static constexpr int STRIDE = SMALL ? 72 : 68;  // 144 B / 272 B per item: conflict-free STS.128
+    static constexpr size_t BYTES = (size_t)P1_ITEMS * STRIDE * sizeof(T);
+};
+
+template <int Q, bool SMALL> struct P1Smem {
+    static constexpr size_t STAGE = Stage<SMALL>::BYTES;
+    static constexpr size_t EXTRA = Q == 7 ? 2 * 64 * 64 * sizeof(int32_t) : 0;  // tmp + I accumulators
+    static constexpr size_t TOTAL = 2 * STAGE + EXTRA;
+};
+
+struct P1Args {
+    const void *counts;  // rows [row_base, ...) of the record, 2^n columns
+    int64_t rowlen;      // 2^n
+    int64_t row_base;    // record row of counts[0]
+    int64_t aH0;         // first tile row group computed (units of 3^Q rows)
+    int64_t naH;         // number of tile row groups computed
+    int64_t out_aH0;     // first tile row group held by the output buffer
+    int64_t C;           // column tiles, 2^(n-Q)
+    Final f;             // f.kind == OUT_INTER: Y1 int32 tile-major
+};
+
+// --- packed loads: 8 consecutive counts -> 4 words (c[2k] | c[2k+1] << 16) ---
+__device__ __forceinline__ void load_packed(const uint16_t *p, uint32_t w[4]) {
+    const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(p));
+    w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
+}
+__device__ __forceinline__ void load_packed(const uint8_t *p, uint32_t w[4]) {
+    const uint2 u = __ldcs(reinterpret_cast<const uint2 *>(p));
+    w[0] = __byte_perm(u.x, 0, 0x4140); w[1] = __byte_perm(u.x, 0, 0x4342);
+    w[2] = __byte_perm(u.y, 0, 0x4140); w[3] = __byte_perm(u.y, 0, 0x4342);
+}
+__device__ __forceinline__ void load_packed(const int32_t *p, uint32_t w[4]) {
+    const int4 a = __ldcs(reinterpret_cast<const int4 *>(p));
+    const int4 b = __ldcs(reinterpret_cast<const int4 *>(p) + 1);
+    w[0] = __byte_perm(a.x, a.y, 0x5410); w[1] = __byte_perm(a.z, a.w, 0x5410);
+    w[2] = __byte_perm(b.x, b.y, 0x5410); w[3] = __byte_perm(b.z, b.w, 0x5410);
+}
+__device__ __forceinline__ void load_packed(const int64_t *p, uint32_t w[4]) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) accI[i] = 0;
+    for (int i = 0; i < 4; ++i) {
+        const longlong2 q = __ldcs(reinterpret_cast<const longlong2 *>(p) + i);
+        w[i] = __byte_perm((uint32_t)q.x, (uint32_t)q.y, 0x5410);
+    }
+}
+// --- wide loads: 8 consecutive counts as int32 ---
+__device__ __forceinline__ void load_wide(const uint16_t *p, int32_t v[8]) {
+    uint32_t w[4];
+    load_packed(p, w);
 #pragma unroll
-    for (int a1 = 0; a1 < 3; ++a1) {
-        Ts x[9][8];
+    for (int k = 0; k < 4; ++k) { v[2 * k] = (int32_t)(w[k] & 0xffff); v[2 * k + 1] = (int32_t)(w[k] >> 16); }
+}
+__device__ __forceinline__ void load_wide(const uint8_t *p, int32_t v[8]) {
+    const uint2 u = __ldcs(reinterpret_cast<const uint2 *>(p));
 #pragma unroll
-        for (int r = 0; r < 9; ++r) {
-            const Tin *p = rowptr(a1 * 9 + r);
-            if (p) {
-                load8<Ts>(p + col0, x[r]);
-            } else {
+    for (int k = 0; k < 4; ++k) { v[k] = (u.x >> (8 * k)) & 0xff; v[4 + k] = (u.y >> (8 * k)) & 0xff; }
+}
+__device__ __forceinline__ void load_wide(const int32_t *p, int32_t v[8]) {
+    const int4 a = __ldcs(reinterpret_cast<const int4 *>(p));
+    const int4 b = __ldcs(reinterpret_cast<const int4 *>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load_wide(const int64_t *p, int32_t v[8]) {
 #pragma unroll
-                for (int c = 0; c < 8; ++c) x[r][c] = 0;
-            }
-        }
-        Ts y[3][4][4];  // [a2][b1 b2][d3]
+    for (int i = 0; i < 4; ++i) {
+        const longlong2 q = __ldcs(reinterpret_cast<const longlong2 *>(p) + i);
+        v[2 * i] = (int32_t)q.x; v[2 * i + 1] = (int32_t)q.y;
+    }
+}
+
+// packed word w = L + 65536 H (|L|,|H|,|L+-H| < 2^15): L - H and L + H
+__device__ __forceinline__ int32_t packed_diff(uint32_t w) {
+    const int32_t L = (int32_t)(int16_t)(w & 0xffffu);  // sign-extended low half
+    return (int32_t)((uint32_t)L * 65537u - w) >> 16;
+}
+__device__ __forceinline__ int32_t packed_sum(uint32_t w) {
+    const int32_t L = (int32_t)(int16_t)(w & 0xffffu);
+    return (int32_t)(w + (uint32_t)L * 65535u) >> 16;
+}
+
+// L1, SMALL mode: 27 rows (j = a1*9 + a2*3 + a3) x 8 columns, qubits
+// (a1,b4) (a2,b5) (a3,b6); b6 is the in-word bit and a3 is streamed.
+// sink(D6, v[16]) receives the 16 values (index D4*4 + D5) of Pauli digit D6
+// as soon as they are final; only the 16 I accumulators stay live.
+template <typename Tin, typename Sink>
+__device__ __forceinline__ void l1_small(const Tin *base, int rowlen, Sink sink) {
+    uint32_t Iacc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Iacc[k] = 0;
+#pragma unroll 1
+    for (int a3 = 0; a3 < 3; ++a3) {
+        uint32_t x[3][3][4];
+#pragma unroll
+        for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+            for (int a2 = 0; a2 < 3; ++a2) load_packed(base + (uint32_t)((a1 * 9 + a2 * 3 + a3) * rowlen), x[a1][a2]);
+        uint32_t y[4][3][2];  // [D4][a2][b5]
 #pragma unroll
         for (int a2 = 0; a2 < 3; ++a2)
 #pragma unroll
-            for (int bb = 0; bb < 4; ++bb)
-                q6to4<Ts>(x[a2 * 3 + 0][2 * bb], x[a2 * 3 + 0][2 * bb + 1], x[a2 * 3 + 1][2 * bb],
-                          x[a2 * 3 + 1][2 * bb + 1], x[a2 * 3 + 2][2 * bb], x[a2 * 3 + 2][2 * bb + 1],
-                          y[a2][bb][0], y[a2][bb][1], y[a2][bb][2], y[a2][bb][3]);
-        Ts z[2][4][4];  // [b1][d2][d3]
+            for (int b5 = 0; b5 < 2; ++b5)
+                q6to4<uint32_t>(x[0][a2][b5], x[0][a2][2 + b5], x[1][a2][b5], x[1][a2][2 + b5], x[2][a2][b5],
+                                x[2][a2][2 + b5], y[0][a2][b5], y[1][a2][b5], y[2][a2][b5], y[3][a2][b5]);
+        int32_t v[16];
 #pragma unroll
-        for (int b1 = 0; b1 < 2; ++b1)
+        for (int D4 = 0; D4 < 4; ++D4) {
+            uint32_t z[4];
+            q6to4<uint32_t>(y[D4][0][0], y[D4][0][1], y[D4][1][0], y[D4][1][1], y[D4][2][0], y[D4][2][1], z[0], z[1],
+                            z[2], z[3]);
 #pragma unroll
-            for (int d3 = 0; d3 < 4; ++d3)
-                q6to4<Ts>(y[0][2 * b1][d3], y[0][2 * b1 + 1][d3], y[1][2 * b1][d3], y[1][2 * b1 + 1][d3],
-                          y[2][2 * b1][d3], y[2][2 * b1 + 1][d3], z[b1][0][d3], z[b1][1][d3], z[b1][2][d3],
-                          z[b1][3][d3]);
-        Ts v[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const Ts s0 = z[0][k >> 2][k & 3], s1 = z[1][k >> 2][k & 3];
-            accI[k] += s0 + s1;
-            v[k] = s0 - s1;
+            for (int D5 = 0; D5 < 4; ++D5) {
+                Iacc[D4 * 4 + D5] += z[D5];
+                v[D4 * 4 + D5] = packed_diff(z[D5]);
+            }
         }
-        sink((a1 + 1) * 16, v);
+        sink(a3 + 1, v);
     }
-    sink(0, accI);
+    int32_t v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = packed_sum(Iacc[k]);
+    sink(0, v);
 }
 
-// 2 qubits: 9 rows x 4 columns -> 16 values (d1*4 + d2)
-template <typename Tin, typename Ts, typename RowPtr>
-__device__ __forceinline__ void transform2(RowPtr rowptr, int64_t col0, Ts out[16]) {
-    Ts x[9][4];
+// L1, WIDE mode (int32 lanes, any shots with 27*shots*3^... < 2^31): same
+// transform without packing; b6 is combined inside the last stage.
+template <typename Tin, typename Sink>
+__device__ __forceinline__ void l1_wide(const Tin *base, int rowlen, Sink sink) {
+    int32_t Iacc[16];
 #pragma unroll
-    for (int r = 0; r < 9; ++r) {
-        const Tin *p = rowptr(r);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) x[r][c] = p ? (Ts)load1<Tin>(p + col0 + c) : (Ts)0;
-    }
-    Ts y[3][2][4];  // [a1][b1][d2]
-#pragma unroll
-    for (int a1 = 0; a1 < 3; ++a1)
-#pragma unroll
-        for (int b1 = 0; b1 < 2; ++b1)
-            q6to4<Ts>(x[a1 * 3 + 0][2 * b1], x[a1 * 3 + 0][2 * b1 + 1], x[a1 * 3 + 1][2 * b1],
-                      x[a1 * 3 + 1][2 * b1 + 1], x[a1 * 3 + 2][2 * b1], x[a1 * 3 + 2][2 * b1 + 1],
-                      y[a1][b1][0], y[a1][b1][1], y[a1][b1][2], y[a1][b1][3]);
-#pragma unroll
-    for (int d2 = 0; d2 < 4; ++d2)
-        q6to4<Ts>(y[0][0][d2], y[0][1][d2], y[1][0][d2], y[1][1][d2], y[2][0][d2], y[2][1][d2], out[0 * 4 + d2],
-                  out[1 * 4 + d2], out[2 * 4 + d2], out[3 * 4 + d2]);
-}
-
-// 1 qubit: 3 rows x 2 columns -> 4 values
-template <typename Tin, typename Ts, typename RowPtr>
-__device__ __forceinline__ void transform1(RowPtr rowptr, int64_t col0, Ts out[4]) {
-    Ts x[3][2];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        const Tin *p = rowptr(r);
-        x[r][0] = p ? (Ts)load1<Tin>(p + col0) : (Ts)0;
-        x[r][1] = p ? (Ts)load1<Tin>(p + col0 + 1) : (Ts)0;
-    }
-    q6to4<Ts>(x[0][0], x[0][1], x[1][0], x[1][1], x[2][0], x[2][1], out[0], out[1], out[2], out[3]);
-}
-
-// ---------------------------------------------------------------------------
-// compile-time fold over QS staged ternary digits for butterfly pattern TS
-// (bit QS-1 of TS = first staged digit).  Digits with t=0 are summed (I),
-// digits with t=1 are kept (X/Y/Z).  out has 3^popc(TS) entries ordered by
-// the kept digits, first staged digit most significant.
-// ---------------------------------------------------------------------------
-template <int QS, int TS> struct Fold {
-    static constexpr int OUT = pow3(popc_c(TS));
-    template <typename Ts, typename Ta> __device__ __forceinline__ static void run(const Ts *x, Ta *out) {
-        constexpr int TOP = (TS >> (QS - 1)) & 1;
-        constexpr int REST = TS & ((1 << (QS - 1)) - 1);
-        constexpr int SUB = pow3(QS - 1);
-        if constexpr (TOP) {
-#pragma unroll
-            for (int a = 0; a < 3; ++a) Fold<QS - 1, REST>::run(x + a * SUB, out + a * Fold<QS - 1, REST>::OUT);
-        } else {
-            Ta s[SUB];
-#pragma unroll
-            for (int i = 0; i < SUB; ++i) s[i] = (Ta)x[i] + (Ta)x[SUB + i] + (Ta)x[2 * SUB + i];
-            Fold<QS - 1, REST>::template run<Ta, Ta>(s, out);
-        }
-    }
-};
-template <int TS> struct Fold<0, TS> {
-    static constexpr int OUT = 1;
-    template <typename Ts, typename Ta> __device__ __forceinline__ static void run(const Ts *x, Ta *out) {
-        out[0] = (Ta)x[0];
-    }
-};
-
-// base-4 staged-digit number of fold output j for pattern TS
-template <int QS, int TS> __host__ __device__ constexpr int fold_slot(int j) {
-    int d = 0, rem = j, kept = popc_c(TS);
-    int div = pow3(kept - 1 < 0 ? 0 : kept - 1);
-    for (int k = QS - 1; k >= 0; --k) {  // from first staged digit
-        int digit = 0;
-        if ((TS >> k) & 1) {
-            digit = rem / div + 1;
-            rem %= div;
-            div = div / 3 > 0 ? div / 3 : 1;
-        }
-        d = d * 4 + digit;
-    }
-    return d;
-}
-
-// ---------------------------------------------------------------------------
-// the fold-pass kernel (Q = 4..7)
-// ---------------------------------------------------------------------------
-template <int Q, typename Ts> struct FoldCfg {
-    static constexpr int QS = (Q - 3 < 3) ? Q - 3 : 3;
-    static constexpr int QP = Q - 3 - QS;  // 0 or 1
-    static constexpr int NRB = pow3(QS);
-    static constexpr int NCG = 1 << (QP + QS);
-    static constexpr int NA_MAX = sizeof(Ts) == 4 ? 432 : 216;
-    static constexpr int TPC = (NA_MAX / (NRB * NCG)) < 1 ? 1 : NA_MAX / (NRB * NCG);
-    static constexpr int NA = TPC * NRB * NCG;
-    static constexpr int SP = 68;  // staging record stride in elements (64 + pad)
-    static constexpr int THREADS = 512;
-    static constexpr int NWARPS = THREADS / 32;
-    static constexpr int NPAIRS = TPC * NCG;
-    static constexpr size_t STAGE_BYTES = (size_t)NA * SP * sizeof(Ts);
-    static_assert(NA <= THREADS, "phase A needs one thread per work item");
-    static_assert(QP == 0 || NPAIRS == NWARPS, "phase digits need one pair per warp");
-};
-
-template <int QS, int TS, int QP, typename Ts, typename Ta>
-__device__ __forceinline__ void phaseB_pair(const Ts *v0, const Ts *v1, void *out, const PassGeom &g, int64_t ob,
-                                            int tP, int round, int lane, Ta *O) {
-    constexpr int OUT = Fold<QS, TS>::OUT;
-    Ta o0[OUT], o1[OUT];
-    Fold<QS, TS>::template run<Ts, Ta>(v0, o0);
-    Fold<QS, TS>::template run<Ts, Ta>(v1, o1);
-    const int di = 2 * lane;
-#pragma unroll
-    for (int j = 0; j < OUT; ++j) {
-        const int dS = fold_slot<QS, TS>(j);
-        if (QP == 0 || tP) {
-            const int dP = QP == 0 ? 0 : round + 1;  // phase digit: X/Y/Z = round + 1
-            const int64_t slot = ((int64_t)dP * (1 << (2 * QS)) + dS) * 64 + di;
-            emit<Ta>(out, g, slot, ob, o0[j]);
-            emit<Ta>(out, g, slot + 1, ob, o1[j]);
-        } else {
-            O[dS * 64 + di] += o0[j];
-            O[dS * 64 + di + 1] += o1[j];
-        }
-    }
-}
-
-template <int Q, typename Tin, typename Ts, typename Ta>
-__global__ void __launch_bounds__(512, 1)
-    fold_pass_kernel(const Tin *__restrict__ in, void *__restrict__ out, const PassGeom g) {
-    using Cfg = FoldCfg<Q, Ts>;
-    constexpr int QS = Cfg::QS, QP = Cfg::QP, NRB = Cfg::NRB, NCG = Cfg::NCG, TPC = Cfg::TPC, SP = Cfg::SP;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Ts *S = reinterpret_cast<Ts *>(smem_raw);
-    Ta *O = reinterpret_cast<Ta *>(smem_raw + Cfg::STAGE_BYTES);  // phase-digit accumulators (QP=1)
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile0 = (int64_t)blockIdx.x * TPC;
-
-    if (QP > 0) {
-        for (int i = tid; i < (1 << (2 * (Q - 1))); i += Cfg::THREADS) O[i] = 0;
-    }
-
-    // phase-A identity of this thread
-    const int ta = tid;
-    const int cg = ta % NCG;
-    const int tl = (ta / NCG) % TPC;
-    const int rb = ta / (NCG * TPC);
-    const int64_t tA = tile0 + tl;
-    const bool activeA = ta < Cfg::NA && tA < g.ntiles;
-    int64_t p = 0, aH = 0, c = 0;
-    if (activeA) {
-        c = tA % g.C;
-        const int64_t rest = tA / g.C;
-        aH = g.aloH + rest % g.nH;
-        p = rest / g.nH;
-    }
-    const int64_t span = g.ahi - g.alo;
-    const Tin *base = in + p * span * g.rowlen;
-    const int64_t col0 = c * ((int64_t)1 << Q) + cg * 8;
-
+    for (int k = 0; k < 16; ++k) Iacc[k] = 0;
 #pragma unroll 1
-    for (int round = 0; round < pow3(QP); ++round) {
-        // ---------------- phase A ----------------
-        if (activeA) {
-            const int64_t a0 = aH * pow3(Q) + ((int64_t)round * NRB + rb) * 27;
-            auto rowptr = [&](int j) -> const Tin * {
-                const int64_t a = a0 + j;
-                return (a >= g.alo && a < g.ahi) ? base + (a - g.alo) * g.rowlen : nullptr;
-            };
-            Ts *rec = S + (size_t)ta * SP;
-            transform3<Tin, Ts>(rowptr, col0, [&](int off, const Ts *v) {
+    for (int a3 = 0; a3 < 3; ++a3) {
+        int32_t y[4][3][4];  // [D4][a2][b5 b6]
 #pragma unroll
-                for (int k = 0; k < 16; k += 4) {
-                    if constexpr (sizeof(Ts) == 4) {
-                        *reinterpret_cast<int4 *>(rec + off + k) = make_int4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+        for (int a2 = 0; a2 < 3; ++a2) {
+            int32_t x[3][8];
+#pragma unroll
+            for (int a1 = 0; a1 < 3; ++a1) load_wide(base + (uint32_t)((a1 * 9 + a2 * 3 + a3) * rowlen), x[a1]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                q6to4<int32_t>(x[0][e], x[0][4 + e], x[1][e], x[1][4 + e], x[2][e], x[2][4 + e], y[0][a2][e],
+                               y[1][a2][e], y[2][a2][e], y[3][a2][e]);
+        }
+        int32_t v[16];
+#pragma unroll
+        for (int D4 = 0; D4 < 4; ++D4) {
+            int32_t z0[4], z1[4];
+            q6to4<int32_t>(y[D4][0][0], y[D4][0][2], y[D4][1][0], y[D4][1][2], y[D4][2][0], y[D4][2][2], z0[0],
+                           z0[1], z0[2], z0[3]);
+            q6to4<int32_t>(y[D4][0][1], y[D4][0][3], y[D4][1][1], y[D4][1][3], y[D4][2][1], y[D4][2][3], z1[0],
+                           z1[1], z1[2], z1[3]);
+#pragma unroll
+            for (int D5 = 0; D5 < 4; ++D5) {
+                Iacc[D4 * 4 + D5] += z0[D5] + z1[D5];
+                v[D4 * 4 + D5] = z0[D5] - z1[D5];
+            }
+        }
+        sink(a3 + 1, v);
+    }
+    sink(0, Iacc);
+}
+
+// L2: the 27 x 8 staged values (rb = a1*9 + a2*3 + a3, g = b1*4 + b2*2 + b3)
+// of one staged column -> sink(D3, v[16]) with v index D1*4 + D2.
+template <typename T, int STRIDE, typename Sink>
+__device__ __forceinline__ void l2_transform(const T *st, Sink sink) {
+    int32_t Iacc[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Iacc[k] = 0;
+#pragma unroll 1
+    for (int a3 = 0; a3 < 3; ++a3) {
+        int32_t y[4][3][4];  // [D1][a2][b2 b3]
+#pragma unroll
+        for (int a2 = 0; a2 < 3; ++a2) {
+            int32_t x[3][8];
+#pragma unroll
+            for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+                for (int g = 0; g < 8; ++g) x[a1][g] = (int32_t)st[((a1 * 9 + a2 * 3 + a3) * 8 + g) * STRIDE];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                q6to4<int32_t>(x[0][e], x[0][4 + e], x[1][e], x[1][4 + e], x[2][e], x[2][4 + e], y[0][a2][e],
+                               y[1][a2][e], y[2][a2][e], y[3][a2][e]);
+        }
+        int32_t v[16];
+#pragma unroll
+        for (int D1 = 0; D1 < 4; ++D1) {
+            int32_t z0[4], z1[4];
+            q6to4<int32_t>(y[D1][0][0], y[D1][0][2], y[D1][1][0], y[D1][1][2], y[D1][2][0], y[D1][2][2], z0[0],
+                           z0[1], z0[2], z0[3]);
+            q6to4<int32_t>(y[D1][0][1], y[D1][0][3], y[D1][1][1], y[D1][1][3], y[D1][2][1], y[D1][2][3], z1[0],
+                           z1[1], z1[2], z1[3]);
+#pragma unroll
+            for (int D2 = 0; D2 < 4; ++D2) {
+                Iacc[D1 * 4 + D2] += z0[D2] + z1[D2];
+                v[D1 * 4 + D2] = z0[D2] - z1[D2];
+            }
+        }
+        sink(a3 + 1, v);
+    }
+    sink(0, Iacc);
+}
+
+// output of one value of the tile: idx in [0, 4^Q); Y1 is tile-major int32
+// (a single-pass plan converts it afterwards with convert_kernel)
+template <int Q>
+__device__ __forceinline__ void p1_emit(const P1Args &a, int64_t tile_out, int idx, int32_t v) {
+    reinterpret_cast<int32_t *>(a.f.out)[(tile_out << (2 * Q)) + idx] = v;
+}
+
+// int32 numerators in natural order -> final theta / int64 numerators
+__global__ void __launch_bounds__(256) convert_kernel(const int32_t *__restrict__ in, int64_t count, const Final f) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        store_final(f, (uint64_t)i, (int64_t)in[i]);
+}
+
+// Staged record of one L1 item: 64 values as [D6][D4*4 + D5] (+ padding), so
+// each sink call is two (int16) or four (int32) 16-byte shared stores.  The
+// L2 thread reading staged column t therefore owns Pauli digits
+// dlo = (D4 D5 D6) = ((t & 15) << 2) | (t >> 4).
+template <int Q, bool SMALL, typename Tin>
+__global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(const P1Args a) {
+    using ST = Stage<SMALL>;
+    using T = typename ST::T;
+    constexpr int STRIDE = ST::STRIDE;
+    constexpr int SUB = Q == 7 ? 6 : 1;
+    constexpr int64_t Q3 = Q == 7 ? 2187 : 729;
+    extern __shared__ __align__(16) unsigned char smem[];
+    int32_t *tmp = reinterpret_cast<int32_t *>(smem + 2 * ST::BYTES);  // [64 res][64 t]
+    int32_t *oi = tmp + 64 * 64;                                        // [64 res][64 t]
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int64_t ntiles = a.naH * a.C;
+    const int64_t my_tiles = (int64_t)blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t S = my_tiles * SUB;
+    const Tin *counts = reinterpret_cast<const Tin *>(a.counts);
+
+    for (int64_t s = 0; s <= S; ++s) {
+        if (warp < P1_L1_WARPS) {
+            if (s < S && tid < P1_ITEMS) {
+                const int64_t t = blockIdx.x + (s / SUB) * (int64_t)gridDim.x;
+                const int sub = (int)(s % SUB);
+                const int r1 = sub >> 1, b1 = sub & 1;
+                const int64_t aH = a.aH0 + t / a.C, c = t % a.C;
+                const int rb = tid >> 3, g = tid & 7;
+                const int64_t row = aH * Q3 + (Q == 7 ? r1 * 729 : 0) + rb * 27 - a.row_base;
+                const int64_t col = (c << Q) + (Q == 7 ? b1 * 64 : 0) + g * 8;
+                const Tin *base = counts + row * a.rowlen + col;
+                T *rec = reinterpret_cast<T *>(smem + (s & 1) * ST::BYTES) + tid * STRIDE;
+                auto stage = [&](int D6, const int32_t(&v)[16]) {
+                    if constexpr (SMALL) {
+#pragma unroll
+                        for (int k = 0; k < 16; k += 8) {
+                            uint4 q;
+                            q.x = __byte_perm(v[k], v[k + 1], 0x5410);
+                            q.y = __byte_perm(v[k + 2], v[k + 3], 0x5410);
+                            q.z = __byte_perm(v[k + 4], v[k + 5], 0x5410);
+                            q.w = __byte_perm(v[k + 6], v[k + 7], 0x5410);
+                            *reinterpret_cast<uint4 *>(rec + D6 * 16 + k) = q;
+                        }
                     } else {
-                        *reinterpret_cast<longlong2 *>(rec + off + k) = make_longlong2(v[k], v[k + 1]);
-                        *reinterpret_cast<longlong2 *>(rec + off + k + 2) = make_longlong2(v[k + 2], v[k + 3]);
+#pragma unroll
+                        for (int k = 0; k < 16; k += 4)
+                            *reinterpret_cast<int4 *>(rec + D6 * 16 + k) = make_int4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+                    }
+                };
+                if constexpr (SMALL) l1_small<Tin>(base, (int)a.rowlen, stage);
+                else l1_wide<Tin>(base, (int)a.rowlen, stage);
+            }
+        } else if (s > 0) {
+            const int64_t sp = s - 1;
+            const int64_t t = blockIdx.x + (sp / SUB) * (int64_t)gridDim.x;
+            const int sub = (int)(sp % SUB);
+            const int r1 = sub >> 1, b1 = sub & 1;
+            const int col = tid - 32 * P1_L1_WARPS;  // staged column 0..63
+            const int dlo = ((col & 15) << 2) | (col >> 4);
+            const int64_t tile_out = (a.aH0 + t / a.C - a.out_aH0) * a.C + t % a.C;
+            l2_transform<T, STRIDE>(reinterpret_cast<const T *>(smem + (sp & 1) * ST::BYTES) + col, [&](int D3, const int32_t(&v)[16]) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int r = k * 4 + D3;  // core digits D1 D2 D3
+                    if constexpr (Q == 6) {
+                        p1_emit<Q>(a, tile_out, r * 64 + dlo, v[k]);
+                    } else if (b1 == 0) {
+                        tmp[r * 64 + col] = v[k];
+                    } else {
+                        const int32_t u = tmp[r * 64 + col];
+                        const int32_t sum = u + v[k];
+                        const int32_t acc = r1 == 0 ? sum : oi[r * 64 + col] + sum;
+                        if (r1 < 2) oi[r * 64 + col] = acc;
+                        else p1_emit<Q>(a, tile_out, r * 64 + dlo, acc);  // top digit I
+                        p1_emit<Q>(a, tile_out, (r1 + 1) * 4096 + r * 64 + dlo, u - v[k]);
                     }
                 }
             });
         }
         __syncthreads();
-        // ---------------- phase A2: butterfly over the NCG column groups ----------------
-        for (int it = tid; it < 16 * NRB * TPC; it += Cfg::THREADS) {
-            const int q = it & 15, rt = it >> 4;
-            Ts w[NCG][4];
+    }
+}
+
+// ===========================================================================
+// vfold: Q <= 3 qubits per pass over a vector axis V
+// ===========================================================================
+// input  X[a][col][v]   a in [xa0, ...) rows of the previous level (only
+//        a in [alo, ahi) hold data, others read as 0), col in [0, 2^R),
+//        v in [0, V)
+// output Y[A - ya0][B][4^Q][v]  for A in [A0, A0 + nA), B in [0, 2^(R-Q))
+// (or, when final, natural Pauli index d * V + v with A = B = 0).
+struct VArgs {
+    const void *in;
+    int64_t V;
+    int64_t ncol;  // 2^R
+    int64_t xa0, alo, ahi;
+    int64_t A0, nA, ya0;
+    int64_t nB;  // 2^(R-Q)
+    Final f;
+};
+
+template <typename Tin>
+__device__ __forceinline__ int64_t vload(const Tin *p) {
+    return (int64_t)__ldcs(p);
+}
+template <> __device__ __forceinline__ int64_t vload<uint8_t>(const uint8_t *p) { return (int64_t)*p; }
+template <> __device__ __forceinline__ int64_t vload<uint16_t>(const uint16_t *p) {
+    return (int64_t)__ldcs(reinterpret_cast<const unsigned short *>(p));
+}
+
+// Loop-invariant strides are re-materialised through an opaque move inside
+// the loop so ptxas does not hoist dozens of 64-bit address products out of
+// it (that alone pushed the Q = 3 kernels to 255 registers with spills).
+__device__ __forceinline__ int64_t opaque(int64_t x) {
+    int64_t y;
+    asm volatile("mov.b64 %0, %1;" : "=l"(y) : "l"(x));
+    return y;
+}
+
+// Q-qubit transform of one (3^Q x 2^Q) block, streamed over the most
+// significant row digit r1: ld(j, s) loads row digits j (< 3^(Q-1), lower
+// digits) x column bits s of the current r1; sink(d, v) receives natural
+// output index d (first qubit most significant).
+template <int Q, typename Ta, typename Ld, typename Sink>
+__device__ __forceinline__ void vblock(Ld ld, Sink sink) {
+    constexpr int H = 1 << (Q - 1);                    // columns per b1
+    constexpr int NL = 1 << (2 * (Q - 1));             // outputs per top digit
+    Ta Iacc[NL];
 #pragma unroll
-            for (int k = 0; k < NCG; ++k) {
-                const Ts *src = S + ((size_t)rt * NCG + k) * SP + 4 * q;
+    for (int k = 0; k < NL; ++k) Iacc[k] = 0;
+#pragma unroll 1
+    for (int r1 = 0; r1 < 3; ++r1) {
+        Ta w[2][NL];  // [b1][lower digits]
 #pragma unroll
-                for (int e = 0; e < 4; ++e) w[k][e] = src[e];
-            }
+        for (int b1 = 0; b1 < 2; ++b1) {
+            if constexpr (Q == 1) {
+                w[b1][0] = ld(r1, 0, b1);
+            } else if constexpr (Q == 2) {
+                Ta x[3][2];
 #pragma unroll
-            for (int h = 1; h < NCG; h <<= 1)
+                for (int j = 0; j < 3; ++j)
 #pragma unroll
-                for (int k = 0; k < NCG; ++k)
-                    if (!(k & h)) {
+                    for (int s = 0; s < 2; ++s) x[j][s] = ld(r1, j, b1 * H + s);
+                q6to4<Ta>(x[0][0], x[0][1], x[1][0], x[1][1], x[2][0], x[2][1], w[b1][0], w[b1][1], w[b1][2], w[b1][3]);
+            } else {
+                Ta u[3][2][4];  // after qubit 3: [r2][b2][D3]
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const Ts u = w[k][e], v = w[k + h][e];
-                            w[k][e] = u + v;
-                            w[k + h][e] = u - v;
-                        }
+                for (int r2 = 0; r2 < 3; ++r2)
+#pragma unroll
+                    for (int b2 = 0; b2 < 2; ++b2) {
+                        Ta x[3][2];
+#pragma unroll
+                        for (int r3 = 0; r3 < 3; ++r3)
+#pragma unroll
+                            for (int b3 = 0; b3 < 2; ++b3) x[r3][b3] = ld(r1, r2 * 3 + r3, b1 * H + b2 * 2 + b3);
+                        q6to4<Ta>(x[0][0], x[0][1], x[1][0], x[1][1], x[2][0], x[2][1], u[r2][b2][0], u[r2][b2][1],
+                                  u[r2][b2][2], u[r2][b2][3]);
                     }
 #pragma unroll
-            for (int k = 0; k < NCG; ++k) {
-                Ts *dst = S + ((size_t)rt * NCG + k) * SP + 4 * q;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) dst[e] = w[k][e];
+                for (int d3 = 0; d3 < 4; ++d3)
+                    q6to4<Ta>(u[0][0][d3], u[0][1][d3], u[1][0][d3], u[1][1][d3], u[2][0][d3], u[2][1][d3],
+                              w[b1][0 * 4 + d3], w[b1][1 * 4 + d3], w[b1][2 * 4 + d3], w[b1][3 * 4 + d3]);
             }
         }
-        __syncthreads();
-        // ---------------- phase B: fold staged digits per butterfly index ----------------
-        for (int pair = warp; pair < Cfg::NPAIRS; pair += Cfg::NWARPS) {
-            const int tl2 = pair / NCG, to = pair % NCG;
-            const int64_t t = tile0 + tl2;
-            if (t >= g.ntiles) continue;
-            const int64_t ob = tile_out_base(g, t);
-            const int tP = to >> QS;
-            const int TS = to & ((1 << QS) - 1);
-            Ts v0[NRB], v1[NRB];
 #pragma unroll
-            for (int r = 0; r < NRB; ++r) {
-                const Ts *src = S + ((size_t)(r * TPC + tl2) * NCG + to) * SP + 2 * lane;
-                v0[r] = src[0];
-                v1[r] = src[1];
-            }
-            switch (TS) {
-#define LRE_CASE(X)                                                                                      \
-    case X:                                                                                              \
-        if constexpr (X < (1 << QS)) phaseB_pair<QS, X, QP, Ts, Ta>(v0, v1, out, g, ob, tP, round, lane, O); \
-        break;
-                LRE_CASE(0)
-                LRE_CASE(1)
-                LRE_CASE(2)
-                LRE_CASE(3)
-                LRE_CASE(4)
-                LRE_CASE(5)
-                LRE_CASE(6)
-                LRE_CASE(7)
-#undef LRE_CASE
-            default: break;
-            }
+        for (int k = 0; k < NL; ++k) {
+            Iacc[k] += w[0][k] + w[1][k];
+            sink((r1 + 1) * NL + k, w[0][k] - w[1][k]);
         }
-        __syncthreads();
     }
-    if (QP > 0 && tile0 < g.ntiles) {  // flush the d1 = I slots accumulated across rounds
-        const int64_t ob = tile_out_base(g, tile0);
-        for (int i = tid; i < (1 << (2 * (Q - 1))); i += Cfg::THREADS) emit<Ta>(out, g, i, ob, O[i]);
+#pragma unroll
+    for (int k = 0; k < NL; ++k) sink(k, Iacc[k]);
+}
+
+template <int Q, typename Tin, typename Ta, bool FINAL>
+__global__ void __launch_bounds__(128, 4) vfold_kernel(const VArgs a) {
+    constexpr int R3 = Q == 1 ? 3 : Q == 2 ? 9 : 27;
+    constexpr int C2 = 1 << Q;
+    constexpr int NOUT = 1 << (2 * Q);
+    constexpr int RL = R3 / 3;  // rows per top digit
+    const int64_t total = a.nA * a.nB * a.V;
+    const Tin *in = reinterpret_cast<const Tin *>(a.in);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t V = opaque(a.V);
+        const int64_t v = t % V;
+        const int64_t rest = t / V;
+        const int64_t B = rest % a.nB;
+        const int64_t A = a.A0 + rest / a.nB;
+        const int64_t row0 = A * R3;
+        const Tin *p0 = in + ((row0 - a.xa0) * a.ncol + B * C2) * V + v;
+        const int64_t rstride = a.ncol * V;
+        auto ld = [&](int r1, int j, int s) -> Ta {
+            const int64_t row = row0 + r1 * RL + j;
+            if (row < a.alo || row >= a.ahi) return (Ta)0;
+            const Tin *rp = p0 + (int64_t)(r1 * RL + j) * rstride;
+            return (Ta)vload<Tin>(rp + (uint32_t)s * (uint32_t)V);
+        };
+        if constexpr (!FINAL) {
+            Ta *out = reinterpret_cast<Ta *>(a.f.out) + ((A - a.ya0) * a.nB + B) * NOUT * V + v;
+            vblock<Q, Ta>(ld, [&](int d, Ta y) { out[(int64_t)d * V] = y; });
+        } else {
+            vblock<Q, Ta>(ld, [&](int d, Ta y) { store_final(a.f, (uint64_t)(d * V + v), (int64_t)y); });
+        }
     }
 }
 
-// ---------------------------------------------------------------------------
-// small passes (Q <= 3): one thread per tile, everything in registers
-// ---------------------------------------------------------------------------
-template <int Q, typename Tin, typename Ta>
-__global__ void __launch_bounds__(128) small_pass_kernel(const Tin *__restrict__ in, void *__restrict__ out,
-                                                          const PassGeom g) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= g.ntiles) return;
-    const int64_t c = t % g.C;
-    const int64_t rest = t / g.C;
-    const int64_t aH = g.aloH + rest % g.nH;
-    const int64_t p = rest / g.nH;
-    const int64_t span = g.ahi - g.alo;
-    const Tin *base = in + p * span * g.rowlen;
-    const int64_t a0 = aH * pow3(Q);
-    auto rowptr = [&](int j) -> const Tin * {
-        const int64_t a = a0 + j;
-        return (a >= g.alo && a < g.ahi) ? base + (a - g.alo) * g.rowlen : nullptr;
-    };
-    const int64_t col0 = c << Q;
-    const int64_t ob = tile_out_base(g, t);
-    if constexpr (Q == 3) {
-        transform3<Tin, Ta>(rowptr, col0, [&](int off, const Ta *v) {
-#pragma unroll
-            for (int k = 0; k < 16; ++k) emit<Ta>(out, g, off + k, ob, v[k]);
-        });
-    } else if constexpr (Q == 2) {
-        Ta v[16];
-        transform2<Tin, Ta>(rowptr, col0, v);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) emit<Ta>(out, g, k, ob, v[k]);
-    } else {
-        Ta v[4];
-        transform1<Tin, Ta>(rowptr, col0, v);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) emit<Ta>(out, g, k, ob, v[k]);
-    }
-}
-
-// ---------------------------------------------------------------------------
+// ===========================================================================
 // host-side planning
-// ---------------------------------------------------------------------------
+// ===========================================================================
 static inline int64_t ipow(int64_t b, int e) {
     int64_t r = 1;
     while (e-- > 0) r *= b;
     return r;
 }
 
-// largest |value| after processing `done` qubits is shots * 3^done
+// |values| after `done` qubits are <= shots * 3^done
 static inline bool fits_i32(int64_t shots, int done) {
     double b = (double)shots;
     for (int i = 0; i < done; ++i) b *= 3.0;
-    return b < 2147483647.0;
+    return b <= 2147483647.0;
 }
 
-std::vector<int> plan_passes(int n, int64_t shots) {
-    std::vector<int> q;
-    if (n <= 7) {
-        q.push_back(n);
-    } else {
-        const int k = (n + 6) / 7;
-        const int base = n / k, extra = n % k;
-        for (int i = 0; i < k; ++i) q.push_back(base + (i < extra ? 1 : 0));
-    }
-    // Q=7 passes need int32 staging (shots * 3^{done+3} < 2^31); otherwise split
-    std::vector<int> out;
-    int done = 0;
-    for (size_t i = 0; i < q.size(); ++i) {
-        int qi = q[i];
-        if (qi == 7 && !fits_i32(shots, done + 3)) {
-            out.push_back(6);
-            done += 6;
-            if (i + 1 < q.size()) q[i + 1] += 1;
-            else q.push_back(1);
-            continue;
-        }
-        out.push_back(qi);
-        done += qi;
-    }
-    return out;
-}
-
-struct PassPlan {
-    std::vector<int> q;
-    std::vector<int64_t> alo, ahi;   // valid input a-range per pass
-    std::vector<size_t> out_bytes;   // intermediate output bytes (non-final)
-    std::vector<int> acc64;          // accumulate in int64
-    std::vector<int> stage64;        // stage in int64
-    size_t ws_bytes = 0;
+struct Pass {
+    int q;            // qubits consumed
+    int kind;         // 0 = tile pass (pass 1), 1 = vfold
+    int small;        // tile pass: packed mode
+    int in_dtype;     // LRE_* of the input
+    int acc64;        // vfold accumulates (and stores intermediates) in int64
+    int64_t alo, ahi; // valid input rows (previous-level units)
+    int64_t A0, nA;   // output row groups computed
+    size_t out_bytes; // intermediate output bytes (0 for the final pass)
 };
 
-PassPlan make_plan(int n, int64_t shots, int64_t w_begin, int64_t w_end) {
-    PassPlan pl;
-    pl.q = plan_passes(n, shots);
+struct Plan {
+    std::vector<Pass> p;
+    size_t ws_bytes = 0;
+    size_t off[2] = {0, 0};  // ping-pong buffers for intermediates
+};
+
+// first-pass width: the tile pass when it applies, else vfold from raw counts
+// vfold passes consume at most two qubits: a thread then needs 36 loads
+// (9 rows x 4 columns) whose 64-bit addresses still fit in registers.
+constexpr int VFOLD_MAX_Q = 2;
+
+static int first_q(int n, int64_t shots) {
+    if (n >= 7 && fits_i32(shots, 7)) return 7;
+    if (n >= 6 && fits_i32(shots, 6)) return 6;
+    return std::min(VFOLD_MAX_Q, n);
+}
+
+Plan make_plan(int n, int64_t shots, int dtype, int64_t w_begin, int64_t w_end) {
+    Plan pl;
     int done = 0;
     int64_t lo = w_begin, hi = w_end;
-    size_t ws = 0;
-    for (size_t i = 0; i < pl.q.size(); ++i) {
-        const int Q = pl.q[i];
-        const int h = n - done - Q;
-        pl.alo.push_back(lo);
-        pl.ahi.push_back(hi);
-        const int64_t q3 = ipow(3, Q);
-        const int64_t loH = lo / q3, hiH = (hi + q3 - 1) / q3;
-        const bool last = i + 1 == pl.q.size();
-        const bool a64 = last || !fits_i32(shots, done + Q);
-        pl.acc64.push_back(a64 ? 1 : 0);
-        pl.stage64.push_back(fits_i32(shots, done + std::min(Q, 3)) ? 0 : 1);
-        if (!last) {
-            const int64_t P = ipow(4, done);
-            const size_t elems = (size_t)ipow(4, Q) * (size_t)P * (size_t)(hiH - loH) * (size_t)ipow(2, h);
-            const size_t bytes = elems * (a64 ? 8 : 4);
-            pl.out_bytes.push_back(bytes);
-            ws += (bytes + 255) & ~(size_t)255;
-        } else {
-            pl.out_bytes.push_back(0);
-        }
-        lo = loH;
-        hi = hiH;
-        done += Q;
+    const int q1 = first_q(n, shots);
+    std::vector<int> qs;
+    qs.push_back(q1);
+    int rem = n - q1;
+    while (rem > 0) {
+        const int q = std::min(VFOLD_MAX_Q, rem);
+        qs.push_back(q);
+        rem -= q;
     }
-    pl.ws_bytes = ws;
+    for (size_t i = 0; i < qs.size(); ++i) {
+        Pass ps{};
+        ps.q = qs[i];
+        ps.kind = (i == 0 && ps.q >= 6) ? 0 : 1;
+        ps.small = (ps.kind == 0 && shots <= SMALL_MAX_SHOTS) ? 1 : 0;
+        ps.in_dtype = i == 0 ? dtype : (pl.p[i - 1].acc64 ? LRE_I64 : LRE_I32);
+        const bool last = i + 1 == qs.size();
+        ps.acc64 = (ps.kind == 1 && (last || !fits_i32(shots, done + ps.q))) ? 1 : 0;
+        ps.alo = lo;
+        ps.ahi = hi;
+        const int64_t q3 = ipow(3, ps.q);
+        ps.A0 = lo / q3;
+        ps.nA = (hi + q3 - 1) / q3 - ps.A0;
+        const int R = n - done;  // remaining qubits before this pass
+        if (!last) {
+            const int64_t nB = ipow(2, R - ps.q);
+            const size_t elems = (size_t)ps.nA * (size_t)nB * (size_t)ipow(4, done + ps.q);
+            ps.out_bytes = elems * (ps.kind == 0 ? 4 : (ps.acc64 ? 8 : 4));
+        }
+        pl.p.push_back(ps);
+        lo = ps.A0;
+        hi = ps.A0 + ps.nA;
+        done += ps.q;
+    }
+    // intermediates alternate between two buffers
+    size_t need[2] = {0, 0};
+    for (size_t i = 0; i + 1 < pl.p.size(); ++i) need[i & 1] = std::max(need[i & 1], pl.p[i].out_bytes);
+    pl.off[0] = 0;
+    pl.off[1] = (need[0] + 255) & ~(size_t)255;
+    pl.ws_bytes = pl.off[1] + ((need[1] + 255) & ~(size_t)255);
+    if (pl.p.size() == 1 && pl.p[0].kind == 0) pl.ws_bytes = (size_t)ipow(4, n) * sizeof(int32_t);
     return pl;
 }
 
-template <typename Tin, typename Ts, typename Ta, int Q>
-static cudaError_t launch_fold(const void *in, void *out, const PassGeom &g, cudaStream_t s) {
-    using Cfg = FoldCfg<Q, Ts>;
-    const size_t smem = Cfg::STAGE_BYTES + (Cfg::QP > 0 ? ((size_t)1 << (2 * (Q - 1))) * sizeof(Ta) : 0);
-    auto kern = fold_pass_kernel<Q, Tin, Ts, Ta>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const int64_t blocks = (g.ntiles + Cfg::TPC - 1) / Cfg::TPC;
-    kern<<<(unsigned)blocks, Cfg::THREADS, smem, s>>>(reinterpret_cast<const Tin *>(in), out, g);
-    count_launch();
-    return cudaGetLastError();
-}
-
-template <typename Tin, typename Ta, int Q>
-static cudaError_t launch_small(const void *in, void *out, const PassGeom &g, cudaStream_t s) {
-    const int64_t blocks = (g.ntiles + 127) / 128;
-    small_pass_kernel<Q, Tin, Ta><<<(unsigned)blocks, 128, 0, s>>>(reinterpret_cast<const Tin *>(in), out, g);
-    count_launch();
-    return cudaGetLastError();
-}
-
-template <typename Tin, typename Ts, typename Ta>
-static cudaError_t dispatch_q(int Q, const void *in, void *out, const PassGeom &g, cudaStream_t s) {
-    switch (Q) {
-    case 1: return launch_small<Tin, Ta, 1>(in, out, g, s);
-    case 2: return launch_small<Tin, Ta, 2>(in, out, g, s);
-    case 3: return launch_small<Tin, Ta, 3>(in, out, g, s);
-    case 4: return launch_fold<Tin, Ts, Ta, 4>(in, out, g, s);
-    case 5: return launch_fold<Tin, Ts, Ta, 5>(in, out, g, s);
-    case 6: return launch_fold<Tin, Ts, Ta, 6>(in, out, g, s);
-    case 7:
-        if constexpr (sizeof(Ts) == 4) return launch_fold<Tin, Ts, Ta, 7>(in, out, g, s);
-        return cudaErrorInvalidValue;
-    default: return cudaErrorInvalidValue;
-    }
-}
-
-template <typename Tin>
-static cudaError_t dispatch_types(int st64, int a64, int Q, const void *in, void *out, const PassGeom &g,
-                                  cudaStream_t s) {
-    if (!a64) return dispatch_q<Tin, int32_t, int32_t>(Q, in, out, g, s);
-    if (!st64) return dispatch_q<Tin, int32_t, int64_t>(Q, in, out, g, s);
-    return dispatch_q<Tin, int64_t, int64_t>(Q, in, out, g, s);
-}
-
-static cudaError_t run_pass(int in_dtype, int st64, int a64, int Q, const void *in, void *out, const PassGeom &g,
-                            cudaStream_t s) {
-    switch (in_dtype) {
-    case LRE_U8: return dispatch_types<uint8_t>(st64, a64, Q, in, out, g, s);
-    case LRE_U16: return dispatch_types<uint16_t>(st64, a64, Q, in, out, g, s);
-    case LRE_I32: return dispatch_types<int32_t>(st64, a64, Q, in, out, g, s);
-    case LRE_I64: return dispatch_types<int64_t>(st64, a64, Q, in, out, g, s);
-    default: return cudaErrorInvalidValue;
-    }
-}
-
+static int g_num_sms = 0;
 static bool g_pow3_ready = false;
 
-static cudaError_t ensure_constants() {
-    if (g_pow3_ready) return cudaSuccess;
-    double t[33];
-    t[0] = 1.0;
-    for (int i = 1; i < 33; ++i) t[i] = t[i - 1] * 3.0;
-    cudaError_t e = cudaMemcpyToSymbol(c_pow3, t, sizeof(t));
-    if (e == cudaSuccess) g_pow3_ready = true;
-    return e;
+static cudaError_t ensure_init() {
+    if (!g_pow3_ready) {
+        double t[33];
+        t[0] = 1.0;
+        for (int i = 1; i < 33; ++i) t[i] = t[i - 1] * 3.0;
+        cudaError_t e = cudaMemcpyToSymbol(c_pow3, t, sizeof(t));
+        if (e != cudaSuccess) return e;
+        g_pow3_ready = true;
+    }
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaError_t e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
-// Run passes [first, last) of the plan for input setting range [w_begin, w_end).
-// full_ws: intermediates use the full-range layout (stage/finish streaming);
-// otherwise they hold only the row groups this range touches (shards).
-static int run_passes(const PassPlan &pl, const PassPlan &full, bool full_ws, size_t first, size_t last,
-                      const void *input, int in_dtype, int n, int64_t shots, void *ws, void *out, int out_kind,
-                      int layout, cudaStream_t stream) {
-    if (ensure_constants() != cudaSuccess) return LRE_ECUDA;
-    const PassPlan &lay = full_ws ? full : pl;
-    std::vector<size_t> offs;
-    size_t off = 0;
-    for (size_t i = 0; i < lay.q.size(); ++i) {
-        offs.push_back(off);
-        off += (lay.out_bytes[i] + 255) & ~(size_t)255;
+template <int Q, bool SMALL, typename Tin>
+static cudaError_t launch_tile(const P1Args &a, cudaStream_t s) {
+    auto kern = tile_pass_kernel<Q, SMALL, Tin>;
+    const size_t smem = P1Smem<Q, SMALL>::TOTAL;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t ntiles = a.naH * a.C;
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * (SMALL ? 2 : 1));
+    kern<<<(unsigned)grid, P1_THREADS, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <int Q, bool SMALL>
+static cudaError_t tile_dtype(int dtype, const P1Args &a, cudaStream_t s) {
+    switch (dtype) {
+    case LRE_U8: return launch_tile<Q, SMALL, uint8_t>(a, s);
+    case LRE_U16: return launch_tile<Q, SMALL, uint16_t>(a, s);
+    case LRE_I32: return launch_tile<Q, SMALL, int32_t>(a, s);
+    case LRE_I64: return launch_tile<Q, SMALL, int64_t>(a, s);
+    default: return cudaErrorInvalidValue;
     }
+}
+
+static cudaError_t run_tile(int q, int small, int dtype, const P1Args &a, cudaStream_t s) {
+#ifdef LRE_ONLY_ONE
+    return launch_tile<7, true, uint16_t>(a, s);
+#else
+    if (q == 7) return small ? tile_dtype<7, true>(dtype, a, s) : tile_dtype<7, false>(dtype, a, s);
+    if (q == 6) return small ? tile_dtype<6, true>(dtype, a, s) : tile_dtype<6, false>(dtype, a, s);
+    return cudaErrorInvalidValue;
+#endif
+}
+
+template <int Q, typename Tin, typename Ta>
+static cudaError_t launch_vfold(const VArgs &a, cudaStream_t s) {
+    const int64_t total = a.nA * a.nB * a.V;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 127) / 128, (int64_t)g_num_sms * 16));
+    if (a.f.kind == OUT_INTER) vfold_kernel<Q, Tin, Ta, false><<<(unsigned)blocks, 128, 0, s>>>(a);
+    else vfold_kernel<Q, Tin, Ta, true><<<(unsigned)blocks, 128, 0, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <typename Tin, typename Ta>
+static cudaError_t vfold_q(int q, const VArgs &a, cudaStream_t s) {
+    switch (q) {
+    case 1: return launch_vfold<1, Tin, Ta>(a, s);
+    case 2: return launch_vfold<2, Tin, Ta>(a, s);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+static cudaError_t run_vfold(int q, int in_dtype, int acc64, const VArgs &a, cudaStream_t s) {
+#ifdef LRE_ONLY_ONE
+    return vfold_q<int32_t, int32_t>(q, a, s);
+#endif
+    if (acc64) {
+        switch (in_dtype) {
+        case LRE_U8: return vfold_q<uint8_t, int64_t>(q, a, s);
+        case LRE_U16: return vfold_q<uint16_t, int64_t>(q, a, s);
+        case LRE_I32: return vfold_q<int32_t, int64_t>(q, a, s);
+        case LRE_I64: return vfold_q<int64_t, int64_t>(q, a, s);
+        default: return cudaErrorInvalidValue;
+        }
+    }
+    switch (in_dtype) {
+    case LRE_U8: return vfold_q<uint8_t, int32_t>(q, a, s);
+    case LRE_U16: return vfold_q<uint16_t, int32_t>(q, a, s);
+    case LRE_I32: return vfold_q<int32_t, int32_t>(q, a, s);
+    case LRE_I64: return vfold_q<int64_t, int32_t>(q, a, s);  // counts bounded by shots < 2^31
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+// Run passes [first, last) of `pl` (computed rows) with intermediates laid out
+// as in `lay` (== pl for one-shot shards; the full-range plan for streaming).
+static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last, const void *counts,
+                      int64_t row_base, int n, int64_t shots, void *ws, void *out, int out_kind, int layout,
+                      cudaStream_t stream) {
+    if (ensure_init() != cudaSuccess) return LRE_ECUDA;
     int done = 0;
-    for (size_t i = 0; i < first; ++i) done += pl.q[i];
-    const void *cur = input;
-    int cur_dtype = in_dtype;
-    if (first > 0) {
-        cur = (const char *)ws + offs[first - 1];
-        cur_dtype = lay.acc64[first - 1] ? LRE_I64 : LRE_I32;
-    }
+    for (size_t i = 0; i < first; ++i) done += pl.p[i].q;
     for (size_t i = first; i < last; ++i) {
-        const int Q = pl.q[i];
-        const int h = n - done - Q;
-        const bool fin = i + 1 == pl.q.size();
-        const int64_t q3 = ipow(3, Q);
-        PassGeom g;
-        g.P = ipow(4, done);
-        g.C = ipow(2, h);
-        // compute only the row groups of this range; address the buffers by `lay`
-        g.alo = lay.alo[i];
-        g.ahi = lay.ahi[i];
-        g.aloH = pl.alo[i] / q3;
-        g.nH = (pl.ahi[i] + q3 - 1) / q3 - g.aloH;
-        if (fin) {
-            g.aHout0 = 0;
-            g.nHout = 1;
+        const Pass &ps = pl.p[i];
+        const Pass &ls = lay.p[i];
+        const bool fin = i + 1 == pl.p.size();
+        const int R = n - done;
+        Final f;
+        f.kind = fin ? (out_kind == LRE_OUT_NUM_I64 ? OUT_NUM : OUT_THETA) : OUT_INTER;
+        f.out = fin ? out : (void *)((char *)ws + lay.off[i & 1]);
+        f.layout = layout;
+        f.n = n;
+        f.shots = shots;
+        f.scale = pow(2.0, -n / 2.0);
+        const void *in = i == 0 ? counts : (const void *)((const char *)ws + lay.off[(i - 1) & 1]);
+        cudaError_t e;
+        if (ps.kind == 0) {
+            P1Args a;
+            a.counts = counts;
+            a.rowlen = (int64_t)1 << n;
+            a.row_base = row_base;
+            a.aH0 = ps.A0;
+            a.naH = ps.nA;
+            a.out_aH0 = fin ? 0 : ls.A0;
+            a.C = ipow(2, R - ps.q);
+            a.f = f;
+            a.f.kind = OUT_INTER;
+            if (fin) a.f.out = ws;  // single-pass plan: int32 tile (natural order), converted below
+            e = run_tile(ps.q, ps.small, ps.in_dtype, a, stream);
+            if (e == cudaSuccess && fin) {
+                const int64_t count = ipow(4, n);
+                const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)g_num_sms * 8);
+                convert_kernel<<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const int32_t *>(ws), count, f);
+                count_launch();
+                e = cudaGetLastError();
+            }
         } else {
-            g.aHout0 = lay.alo[i] / q3;
-            g.nHout = (lay.ahi[i] + q3 - 1) / q3 - g.aHout0;
+            VArgs a;
+            a.in = in;
+            a.V = ipow(4, done);
+            a.ncol = ipow(2, R);
+            a.xa0 = i == 0 ? row_base : ls.alo;
+            a.alo = ps.alo;
+            a.ahi = ps.ahi;
+            a.A0 = ps.A0;
+            a.nA = ps.nA;
+            a.ya0 = fin ? 0 : ls.A0;
+            a.nB = ipow(2, R - ps.q);
+            a.f = f;
+            e = run_vfold(ps.q, ps.in_dtype, ps.acc64, a, stream);
         }
-        if (i == 0) {  // the counts buffer holds exactly [w_begin, w_end)
-            g.alo = pl.alo[0];
-            g.ahi = pl.ahi[0];
-        }
-        g.RCout = g.P * g.nHout * g.C;
-        g.ntiles = g.P * g.nH * g.C;
-        g.rowlen = g.C << Q;
-        g.Q = Q;
-        g.final_pass = fin ? 1 : 0;
-        g.out_kind = out_kind;
-        g.layout = layout;
-        g.n = n;
-        g.shots = shots;
-        g.scale = pow(2.0, -n / 2.0);
-        void *dst = fin ? out : (void *)((char *)ws + offs[i]);
-        cudaError_t e = run_pass(cur_dtype, pl.stage64[i], pl.acc64[i], Q, cur, dst, g, stream);
         if (e != cudaSuccess) return e == cudaErrorInvalidValue ? LRE_EUNSUPPORTED : LRE_ECUDA;
-        if (!fin) {
-            cur = dst;
-            cur_dtype = pl.acc64[i] ? LRE_I64 : LRE_I32;
-        }
-        done += Q;
+        done += ps.q;
     }
     return LRE_OK;
 }
 
 int step1_impl(const void *counts, int dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end, void *ws,
                size_t ws_bytes, void *out, int out_kind, int layout, cudaStream_t stream) {
-    const PassPlan pl = make_plan(n, shots, w_begin, w_end);
+    const Plan pl = make_plan(n, shots, dtype, w_begin, w_end);
     if (ws_bytes < pl.ws_bytes || (pl.ws_bytes && !ws)) return LRE_ENOMEM;
-    return run_passes(pl, pl, false, 0, pl.q.size(), counts, dtype, n, shots, ws, out, out_kind, layout, stream);
+    return run_passes(pl, pl, 0, pl.p.size(), counts, w_begin, n, shots, ws, out, out_kind, layout, stream);
 }
 
-// pass 1 of a setting chunk into the full-range workspace
+// pass 1 of a setting chunk into the full-range workspace (streaming records)
 int step1_stage_impl(const void *counts, int dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end, void *ws,
                      size_t ws_bytes, cudaStream_t stream) {
-    const PassPlan full = make_plan(n, shots, 0, ipow(3, n));
-    if (full.q.size() < 2) return LRE_EUNSUPPORTED;
+    const Plan full = make_plan(n, shots, dtype, 0, ipow(3, n));
+    if (full.p.size() < 2) return LRE_EUNSUPPORTED;
     if (ws_bytes < full.ws_bytes || !ws) return LRE_ENOMEM;
-    const PassPlan pl = make_plan(n, shots, w_begin, w_end);
-    if (pl.q != full.q) return LRE_EINVAL;
-    return run_passes(pl, full, true, 0, 1, counts, dtype, n, shots, ws, nullptr, 0, 0, stream);
+    const Plan pl = make_plan(n, shots, dtype, w_begin, w_end);
+    return run_passes(pl, full, 0, 1, counts, w_begin, n, shots, ws, nullptr, 0, 0, stream);
 }
 
 // passes 2.. over the full-range workspace
 int step1_finish_impl(void *ws, size_t ws_bytes, int n, int64_t shots, void *out, int out_kind, int layout,
                       cudaStream_t stream) {
-    const PassPlan full = make_plan(n, shots, 0, ipow(3, n));
-    if (full.q.size() < 2) return LRE_EUNSUPPORTED;
+    // the count dtype only affects pass 1; any value gives the same later passes
+    const Plan full = make_plan(n, shots, LRE_I64, 0, ipow(3, n));
+    if (full.p.size() < 2) return LRE_EUNSUPPORTED;
     if (ws_bytes < full.ws_bytes || !ws) return LRE_ENOMEM;
-    return run_passes(full, full, true, 1, full.q.size(), nullptr, 0, n, shots, ws, out, out_kind, layout, stream);
+    return run_passes(full, full, 1, full.p.size(), nullptr, 0, n, shots, ws, out, out_kind, layout, stream);
 }
 
-int step1_num_passes(int n, int64_t shots) { return (int)plan_passes(n, shots).size(); }
+int step1_num_passes(int n, int64_t shots) { return (int)make_plan(n, shots, LRE_I64, 0, ipow(3, n)).p.size(); }
 
 size_t step1_workspace(int n, int64_t shots, int64_t w_begin, int64_t w_end) {
-    return make_plan(n, shots, w_begin, w_end).ws_bytes;
+    return make_plan(n, shots, LRE_I64, w_begin, w_end).ws_bytes;
 }
 
-int64_t shard_quantum(int n, int64_t shots) { return ipow(3, plan_passes(n, shots)[0]); }
+// setting shards must align to the first pass's row groups; 3^min(n,7) works
+// for every plan (3^q1 divides it)
+int64_t shard_quantum(int n, int64_t /*shots*/) { return ipow(3, std::min(n, 7)); }
 
 }  // namespace lre

@@ -5,7 +5,7 @@
 // X/Y mask m the reference gathers v[a] = theta[(m,a)] * (-i)^popcount(a&m),
 // runs a complex WHT of length 2^n and writes mu[r, r^m].
 //
-// B200 design (DESIGN.md §4): with w[a] = theta[(m,a)] * (-1)^floor(pc(a&m)/2)
+// B200 design (DESIGN.md §5): with w[a] = theta[(m,a)] * (-1)^floor(pc(a&m)/2)
 // and the real WHT F = H w, the complex WHT splits exactly as
 //     mu[r, r^m] = 2^{-n/2} ( (F[r] + F[r^m]) / 2  -  i (F[r] - F[r^m]) / 2 ),
 // so one real fp64 transform per mask replaces the complex one.  A CTA owns
@@ -46,8 +46,8 @@ __device__ __forceinline__ void wht_round(double *buf, int Dp, int logd, int mpc
     }
 }
 
-__global__ void __launch_bounds__(1024) assemble_kernel(const double *__restrict__ theta, int logd, int64_t m_begin,
-                                                        int64_t S, int mpc, double scale_half,
+__global__ void __launch_bounds__(1024) assemble_kernel(const double *__restrict__ theta, int layout, int logd,
+                                                        int64_t m_begin, int64_t S, int mpc, double scale_half,
                                                         double2 *__restrict__ mu) {
     extern __shared__ double sbuf[];
     const int d = 1 << logd;
@@ -57,7 +57,12 @@ __global__ void __launch_bounds__(1024) assemble_kernel(const double *__restrict
     for (int e = threadIdx.x; e < mpc * d; e += blockDim.x) {
         const int ml = e >> logd, a = e & (d - 1);
         const uint32_t m = (uint32_t)(m_begin + mloc0 + ml);
-        double v = __ldcs(theta + (mloc0 + ml) * (int64_t)d + a);
+        // NATURAL: full theta, gathered at the natural index of (m, a); the CTA's
+        // consecutive masks cover all digits of the low qubits, so the gather
+        // reads whole lines.  MASK_MAJOR: the slice of masks [m_begin, m_end).
+        const int64_t idx = layout == LRE_LAYOUT_NATURAL ? (int64_t)ma_to_natural(m, (uint32_t)a)
+                                                         : (mloc0 + ml) * (int64_t)d + a;
+        double v = __ldg(theta + idx);
         if ((__popc((uint32_t)a & m) >> 1) & 1) v = -v;
         sbuf[ml * Dp + padix(a)] = v;
     }
@@ -86,7 +91,8 @@ __global__ void __launch_bounds__(1024) assemble_kernel(const double *__restrict
     }
 }
 
-int assemble_impl(const double *theta_mm, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s) {
+int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu,
+                  cudaStream_t s) {
     const int64_t S = m_end - m_begin;
     const int64_t d = (int64_t)1 << n;
     if (n < 1 || n > 14) return LRE_EUNSUPPORTED;
@@ -99,7 +105,7 @@ int assemble_impl(const double *theta_mm, int n, int64_t m_begin, int64_t m_end,
     cudaError_t e = cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return LRE_ECUDA;
     const double scale_half = 0.5 * pow(2.0, -n / 2.0);
-    assemble_kernel<<<(unsigned)(S / mpc), threads, smem, s>>>(theta_mm, n, m_begin, S, mpc, scale_half,
+    assemble_kernel<<<(unsigned)(S / mpc), threads, smem, s>>>(theta, layout, n, m_begin, S, mpc, scale_half,
                                                               reinterpret_cast<double2 *>(mu));
     count_launch();
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;

@@ -80,8 +80,8 @@ class DeviceCompute:
         d = 1 << self.n
         self.lib.call("lre_finalize", self.recv.data_ptr(), self.n, self.shots, self.lib.MASK_MAJOR,
                       self.m_lo * d, self.m_hi * d, self.theta.data_ptr(), self.stream().cuda_stream)
-        self.lib.call("lre_assemble", self.theta.data_ptr(), self.n, self.m_lo, self.m_hi, self.mu.data_ptr(),
-                      self.stream().cuda_stream)
+        self.lib.call("lre_assemble", self.theta.data_ptr(), self.lib.MASK_MAJOR, self.n, self.m_lo, self.m_hi,
+                      self.mu.data_ptr(), self.stream().cuda_stream)
         return self.mu
 
 

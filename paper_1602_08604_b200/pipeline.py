@@ -103,8 +103,13 @@ def to_device_record(record_or_source, device=None, stream=None) -> DeviceRecord
 class LREPlan:
     """Preallocated HBM buffers and the launch sequence of one reconstruction.
 
-    step1: counts -> theta (MASK_MAJOR fp64), 1-3 fold-pass launches;
-    step2: theta -> mu (row-major complex128), 1 launch.
+    step1: counts -> theta (natural order, fp64): the tile pass plus 2-qubit
+    vector passes (lre_step1, DESIGN.md §3);
+    step2: theta -> mu (row-major complex128), 1 launch (lre_assemble).
+
+    ``mu`` lives inside the step-(i) workspace when that is large enough (the
+    workspace is dead once theta is final), which is what lets an n = 14
+    record (157 GB of uint16 counts) and the whole pipeline share one B200.
     """
 
     def __init__(self, n: int, shots: int, device=None, with_mu: bool = True):
@@ -118,16 +123,17 @@ class LREPlan:
         ws = ctypes.c_size_t(0)
         _lib.check(L.lre_step1_workspace(self.n, self.shots, 0, 3**self.n, ctypes.byref(ws)), "lre_step1_workspace")
         self.ws_bytes = int(ws.value)
-        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=self.device)
-        self.theta_mm = torch.empty(4**self.n, dtype=torch.float64, device=self.device)
         d = 1 << self.n
-        self.mu = torch.empty((d, d), dtype=torch.complex128, device=self.device) if with_mu else None
+        mu_bytes = 16 * d * d if with_mu else 0
+        self.ws = torch.empty(max(self.ws_bytes, mu_bytes, 256), dtype=torch.uint8, device=self.device)
+        self.theta = torch.empty(4**self.n, dtype=torch.float64, device=self.device)
+        self.mu = self.ws[:mu_bytes].view(torch.complex128).view(d, d) if with_mu else None
         self.passes = int(L.lre_step1_num_passes(self.n, self.shots))
 
     def step1(self, counts, count_dtype: int, stream) -> None:
         _lib.call("lre_step1", counts.data_ptr(), count_dtype, self.n, self.shots, 0, 3**self.n,
-                  self.ws.data_ptr(), self.ws_bytes, self.theta_mm.data_ptr(), _lib.OUT_THETA_F64,
-                  _lib.MASK_MAJOR, stream.cuda_stream)
+                  self.ws.data_ptr(), self.ws_bytes, self.theta.data_ptr(), _lib.OUT_THETA_F64,
+                  _lib.NATURAL, stream.cuda_stream)
 
     def stage(self, chunk, count_dtype: int, w_begin: int, w_end: int, stream) -> None:
         _lib.call("lre_step1_stage", chunk.data_ptr(), count_dtype, self.n, self.shots, int(w_begin), int(w_end),
@@ -135,32 +141,16 @@ class LREPlan:
 
     def finish(self, stream) -> None:
         _lib.call("lre_step1_finish", self.ws.data_ptr(), self.ws_bytes, self.n, self.shots,
-                  self.theta_mm.data_ptr(), _lib.OUT_THETA_F64, _lib.MASK_MAJOR, stream.cuda_stream)
+                  self.theta.data_ptr(), _lib.OUT_THETA_F64, _lib.NATURAL, stream.cuda_stream)
 
     def step2(self, stream) -> None:
         d = 1 << self.n
-        _lib.call("lre_assemble", self.theta_mm.data_ptr(), self.n, 0, d, self.mu.data_ptr(), stream.cuda_stream)
+        _lib.call("lre_assemble", self.theta.data_ptr(), _lib.NATURAL, self.n, 0, d, self.mu.data_ptr(),
+                  stream.cuda_stream)
 
     def run(self, counts, count_dtype: int, stream) -> None:
         self.step1(counts, count_dtype, stream)
         self.step2(stream)
-
-    def theta_natural(self, stream, out=None):
-        torch = _torch()
-        out = torch.empty_like(self.theta_mm) if out is None else out
-        _lib.call("lre_theta_relayout", self.theta_mm.data_ptr(), _lib.MASK_MAJOR, self.n, out.data_ptr(),
-                  stream.cuda_stream)
-        return out
-
-
-def _theta_mm_from(theta, n, device, stream):
-    """natural-order theta (numpy or tensor) -> mask-major device tensor."""
-    torch = _torch()
-    t = theta if isinstance(theta, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(theta, dtype=np.float64))
-    t = t.to(device=device, dtype=torch.float64).contiguous()
-    mm = torch.empty_like(t)
-    _lib.call("lre_theta_relayout", t.data_ptr(), _lib.NATURAL, n, mm.data_ptr(), stream.cuda_stream)
-    return mm
 
 
 # ---------------------------------------------------------------------------
@@ -200,10 +190,11 @@ def step_two_assemble(theta, workers: int = 1, *, device=None, as_tensor: bool =
         raise NotImplementedError(f"dense assembly is built for n <= {DENSE_PIPELINE_MAX_QUBITS}")
     dev = theta.device if isinstance(theta, torch.Tensor) and theta.is_cuda else _device(device)
     stream = torch.cuda.current_stream(dev)
-    mm = _theta_mm_from(theta, n, dev, stream)
+    t = theta if isinstance(theta, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(theta, dtype=np.float64))
+    t = t.to(device=dev, dtype=torch.float64).contiguous()
     d = 1 << n
     mu = torch.empty((d, d), dtype=torch.complex128, device=dev)
-    _lib.call("lre_assemble", mm.data_ptr(), n, 0, d, mu.data_ptr(), stream.cuda_stream)
+    _lib.call("lre_assemble", t.data_ptr(), _lib.NATURAL, n, 0, d, mu.data_ptr(), stream.cuda_stream)
     return mu if as_tensor else mu.cpu().numpy()
 
 
@@ -275,8 +266,7 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
 
     Validation happens before the timer, as in the reference.  ``timings``
     has the reference keys t_step1_s / t_step2_s / t_step3_s / t_total_s /
-    threads / kernel, measured with CUDA events, plus gpus and
-    t_theta_export_s (natural-order theta export, outside the hot path).
+    threads / kernel, measured with CUDA events, plus gpus.
     """
     _check_kernel(kernel)
     torch = _torch()
@@ -301,7 +291,7 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
     else:
         rho, evals = plan.mu, None
     ev[3].record(stream)
-    theta = plan.theta_natural(stream)
+    theta = plan.theta
     ev[4].record(stream)
     ev[4].synchronize()
     t1 = ev[0].elapsed_time(ev[1]) / 1e3
@@ -315,7 +305,6 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
         "threads": workers,
         "kernel": kernel,
         "gpus": 1,
-        "t_theta_export_s": ev[3].elapsed_time(ev[4]) / 1e3,
     }
     mu = plan.mu
     if not as_tensor:
