@@ -162,33 +162,55 @@ def traffic_from_profiles(n: int):
         return None
 
 
-def e2e_host(plan, host_counts, n, shots, mu_host, chunk_rows, steps, warmup, torch, lre_dtype):
-    """Public streaming API from pinned host counts: H2D chunks (copy stream)
-    overlapped with the first fold pass, then the remaining passes, assembly
-    and the D2H of mu, all inside the timed region."""
-    from paper_1602_08604_b200 import _lib
+def host_record(counts, chunk_rows, torch):
+    """Copy the device record to HOST memory in slabs of whole chunks: pinned
+    when the host allows it (a 157 GB single pinned allocation is refused on
+    these boxes), otherwise pageable.  Returns ([(lo, hi, tensor)], pinned)."""
+    rows = counts.shape[0]
+    slab_rows = chunk_rows * 4
+    for pin in (True, False):
+        slabs = []
+        try:
+            for lo in range(0, rows, slab_rows):
+                hi = min(rows, lo + slab_rows)
+                t = torch.empty((hi - lo, counts.shape[1]), dtype=counts.dtype, pin_memory=pin)
+                t.copy_(counts[lo:hi])
+                slabs.append((lo, hi, t))
+            return slabs, pin
+        except Exception:
+            del slabs
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+    raise MemoryError("could not stage the record in host memory")
 
+
+def e2e_host(plan, slabs, n, mu_host, chunk_rows, steps, warmup, torch, lre_dtype):
+    """Public streaming API from HOST counts: H2D chunks (copy stream)
+    overlapped with the first pass (lre_step1_stage), then the remaining
+    passes (lre_step1_finish), assembly (lre_assemble) and the D2H of mu, all
+    inside the timed region."""
     dev = plan.device
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
-    total = 3**n
-    bufs = [torch.empty((chunk_rows, 1 << n), dtype=host_counts.dtype, device=dev) for _ in range(2)]
+    width = slabs[0][2].shape[1]
+    bufs = [torch.empty((chunk_rows, width), dtype=slabs[0][2].dtype, device=dev) for _ in range(2)]
     ev_copy = [torch.cuda.Event() for _ in range(2)]
     ev_used = [torch.cuda.Event() for _ in range(2)]
 
     def one():
         k = 0
-        for lo in range(0, total, chunk_rows):
-            hi = min(total, lo + chunk_rows)
-            b = k % 2
-            copy.wait_event(ev_used[b])
-            with torch.cuda.stream(copy):
-                bufs[b][: hi - lo].copy_(host_counts[lo:hi], non_blocking=True)
-                ev_copy[b].record(copy)
-            comp.wait_event(ev_copy[b])
-            plan.stage(bufs[b], lre_dtype, lo, hi, comp)
-            ev_used[b].record(comp)
-            k += 1
+        for s_lo, s_hi, slab in slabs:
+            for lo in range(s_lo, s_hi, chunk_rows):
+                hi = min(s_hi, lo + chunk_rows)
+                b = k % 2
+                copy.wait_event(ev_used[b])
+                with torch.cuda.stream(copy):
+                    bufs[b][: hi - lo].copy_(slab[lo - s_lo:hi - s_lo], non_blocking=True)
+                    ev_copy[b].record(copy)
+                comp.wait_event(ev_copy[b])
+                plan.stage(bufs[b], lre_dtype, lo, hi, comp)
+                ev_used[b].record(comp)
+                k += 1
         plan.finish(comp)
         plan.step2(comp)
         mu_host.copy_(plan.mu, non_blocking=True)
@@ -282,7 +304,11 @@ def run_b200(args):
     t_pass1 = e[0].elapsed_time(e[1]) / 1e3 / k
     t_rest1 = e[1].elapsed_time(e[2]) / 1e3 / k
     t_asm = e[2].elapsed_time(e[3]) / 1e3 / k
-    pass1_bytes = c * 6.0**n  # algorithmic: every count read once
+    pass1_bytes = c * 6.0**n  # algorithmic: every count read once (the Y1 write is not counted)
+    q1 = min(n, 7)
+    tma = counts.dtype == torch.uint16 and shots <= 1213 and n >= 6 and os.environ.get("LRE_NO_TMA") != "1"
+    p1_name = (f"tile_tma_kernel<{q1}> (pass 1, TMA ring)" if tma else f"tile_pass_kernel<{q1}> (pass 1, LDG)") \
+        if n >= 6 else "vfold_kernel (pass 1)"
     achieved = pass1_bytes / t_pass1 / 1e9
     traffic = traffic_from_profiles(n)
     whole = algorithmic_bytes(n, c) / t_step / 1e9
@@ -292,23 +318,26 @@ def run_b200(args):
     if not args.no_e2e:
         host_bytes = counts.numel() * c
         avail = _mem_available()
-        if avail is None or avail > host_bytes + (24 << 30):
-            host = torch.empty(tuple(counts.shape), dtype=counts.dtype, pin_memory=True)
-            host.copy_(counts)
-            mu_host = torch.empty(tuple(plan.mu.shape), dtype=plan.mu.dtype, pin_memory=True)
-            del rec
-            counts = None
-            torch.cuda.empty_cache()
-            chunk = max(1, (2 << 30) // (host.shape[1] * c))
-            q = int(_lib.load().lre_shard_quantum(n))
-            chunk = max(q, chunk // q * q)
-            ksteps = max(1, min(args.steps, args.e2e_steps))
-            t_e2e, wall_e2e = e2e_host(plan, host, n, shots, mu_host, chunk, ksteps, 1, torch, lre_dtype)
-            e2e = {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(host_bytes),
-                   "d2h_bytes_per_step": int(mu_host.numel() * mu_host.element_size()),
-                   "wall_s_per_step": wall_e2e, "api": "LREPlan.stage/finish/step2 (lre_step1_stage/finish, "
-                                                       "lre_assemble) from pinned host counts"}
-            del host, mu_host
+        if avail is None or avail > host_bytes + (16 << 30):
+            try:
+                q = int(_lib.load().lre_shard_quantum(n))
+                chunk = max(1, (2 << 30) // (counts.shape[1] * c))
+                chunk = max(q, chunk // q * q)
+                slabs, pinned = host_record(counts, chunk, torch)
+                mu_host = torch.empty(tuple(plan.mu.shape), dtype=plan.mu.dtype, pin_memory=True)
+                del rec
+                counts = None
+                torch.cuda.empty_cache()
+                ksteps = max(1, min(args.steps, args.e2e_steps))
+                t_e2e, wall_e2e = e2e_host(plan, slabs, n, mu_host, chunk, ksteps, 1, torch, lre_dtype)
+                e2e = {"value": t_e2e, "unit": "s", "h2d_bytes_per_step": int(host_bytes),
+                       "d2h_bytes_per_step": int(mu_host.numel() * mu_host.element_size()),
+                       "wall_s_per_step": wall_e2e, "host_memory": "pinned" if pinned else "pageable",
+                       "steps": ksteps,
+                       "api": "LREPlan.stage/finish/step2 (lre_step1_stage/finish, lre_assemble) from host counts"}
+                del slabs, mu_host
+            except Exception as exc:  # keep the device-side line even if the host side fails
+                e2e = {"value": None, "unit": "s", "error": f"{type(exc).__name__}: {str(exc)[:200]}"}
         else:
             e2e = {"value": None, "unit": "s", "skipped": f"host RAM {avail >> 30} GiB < record {host_bytes >> 30} GiB"}
 
@@ -332,7 +361,7 @@ def run_b200(args):
                    "passes": plan.passes,
                    "vs_baseline_ref": "paper GTX 780 steps (i)+(ii) at n=14, 2.86 h (PAPER.md:167,169)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "fold pass 1 (fold_pass_kernel<7,u16>)",
+                     "traffic": traffic, "kernel": p1_name,
                      "algorithmic_bytes_per_launch": pass1_bytes, "avg_launch_s": t_pass1, "peak_kind": peak_kind},
         "whole_path": {"algorithmic_bytes": algorithmic_bytes(n, c), "achieved_GBps": whole, "frac": whole / peak,
                        "t_pass1_s": t_pass1, "t_pass2_s": t_rest1, "t_assemble_s": t_asm},

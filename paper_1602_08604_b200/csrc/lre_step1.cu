@@ -24,8 +24,13 @@
 // 3^{zc} (pipeline.py:138, records.py:64).
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "lre_internal.cuh"
 
@@ -76,8 +81,8 @@ __device__ __forceinline__ void store_final(const Final &f, uint64_t nat, int64_
 // SMALL mode (shots <= 1213): L1 keeps two outcomes per 32-bit word
 // (w = lo + 65536*hi, exact mod 2^32) so each add works on two counts; the
 // staged values fit int16 (|v| <= 27*shots).
-constexpr int P1_L1_WARPS = 7;
-constexpr int P1_L2_WARPS = 2;
+constexpr int P1_L1_WARPS = 7;  // 216 L1 items per sub-tile
+constexpr int P1_L2_WARPS = 2;  // 64 staged columns
 constexpr int P1_THREADS = 32 * (P1_L1_WARPS + P1_L2_WARPS);
 constexpr int P1_ITEMS = 216;
 constexpr int SMALL_MAX_SHOTS = 1213;  // 27 * shots <= 32767
@@ -167,8 +172,8 @@ __device__ __forceinline__ int32_t packed_sum(uint32_t w) {
 // (a1,b4) (a2,b5) (a3,b6); b6 is the in-word bit and a3 is streamed.
 // sink(D6, v[16]) receives the 16 values (index D4*4 + D5) of Pauli digit D6
 // as soon as they are final; only the 16 I accumulators stay live.
-template <typename Tin, typename Sink>
-__device__ __forceinline__ void l1_small(const Tin *base, int rowlen, Sink sink) {
+template <typename RowLd, typename Sink>
+__device__ __forceinline__ void l1_small(RowLd ld, Sink sink) {
     uint32_t Iacc[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) Iacc[k] = 0;
@@ -178,7 +183,7 @@ __device__ __forceinline__ void l1_small(const Tin *base, int rowlen, Sink sink)
 #pragma unroll
         for (int a1 = 0; a1 < 3; ++a1)
 #pragma unroll
-            for (int a2 = 0; a2 < 3; ++a2) load_packed(base + (uint32_t)((a1 * 9 + a2 * 3 + a3) * rowlen), x[a1][a2]);
+            for (int a2 = 0; a2 < 3; ++a2) ld(a1 * 9 + a2 * 3 + a3, x[a1][a2]);
         uint32_t y[4][3][2];  // [D4][a2][b5]
 #pragma unroll
         for (int a2 = 0; a2 < 3; ++a2)
@@ -208,8 +213,8 @@ __device__ __forceinline__ void l1_small(const Tin *base, int rowlen, Sink sink)
 
 // L1, WIDE mode (int32 lanes, any shots with 27*shots*3^... < 2^31): same
 // transform without packing; b6 is combined inside the last stage.
-template <typename Tin, typename Sink>
-__device__ __forceinline__ void l1_wide(const Tin *base, int rowlen, Sink sink) {
+template <typename RowLd, typename Sink>
+__device__ __forceinline__ void l1_wide(RowLd ld, Sink sink) {
     int32_t Iacc[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) Iacc[k] = 0;
@@ -220,7 +225,7 @@ __device__ __forceinline__ void l1_wide(const Tin *base, int rowlen, Sink sink) 
         for (int a2 = 0; a2 < 3; ++a2) {
             int32_t x[3][8];
 #pragma unroll
-            for (int a1 = 0; a1 < 3; ++a1) load_wide(base + (uint32_t)((a1 * 9 + a2 * 3 + a3) * rowlen), x[a1]);
+            for (int a1 = 0; a1 < 3; ++a1) ld(a1 * 9 + a2 * 3 + a3, x[a1]);
 #pragma unroll
             for (int e = 0; e < 4; ++e)
                 q6to4<int32_t>(x[0][e], x[0][4 + e], x[1][e], x[1][4 + e], x[2][e], x[2][4 + e], y[0][a2][e],
@@ -286,24 +291,100 @@ __device__ __forceinline__ void l2_transform(const T *st, Sink sink) {
     sink(0, Iacc);
 }
 
-// output of one value of the tile: idx in [0, 4^Q); Y1 is tile-major int32
-// (a single-pass plan converts it afterwards with convert_kernel)
-template <int Q>
-__device__ __forceinline__ void p1_emit(const P1Args &a, int64_t tile_out, int idx, int32_t v) {
-    reinterpret_cast<int32_t *>(a.f.out)[(tile_out << (2 * Q)) + idx] = v;
-}
-
 // int32 numerators in natural order -> final theta / int64 numerators
 __global__ void __launch_bounds__(256) convert_kernel(const int32_t *__restrict__ in, int64_t count, const Final f) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
         store_final(f, (uint64_t)i, (int64_t)in[i]);
 }
 
-// Staged record of one L1 item: 64 values as [D6][D4*4 + D5] (+ padding), so
-// each sink call is two (int16) or four (int32) 16-byte shared stores.  The
-// L2 thread reading staged column t therefore owns Pauli digits
-// dlo = (D4 D5 D6) = ((t & 15) << 2) | (t >> 4).
-template <int Q, bool SMALL, typename Tin>
+// Staged record of one L1 item: 64 values (+ padding) at position
+//   col = (D4 >> 1) * 32 + D6 * 8 + (D4 & 1) * 4 + D5
+// so each sink call is two 8-value chunks (one 16-byte shared store each in
+// SMALL mode) and the L2 warp reading columns [32w, 32w + 32) owns the 32
+// consecutive Pauli indices dlo = D4*16 + D5*4 + D6 in [32w, 32w + 32): its
+// global stores are whole 128-byte lines.
+template <bool SMALL>
+__device__ __forceinline__ void stage_record(typename Stage<SMALL>::T *rec, int D6, const int32_t (&v)[16]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int k = 8 * h;
+        if constexpr (SMALL) {
+            uint4 q;
+            q.x = __byte_perm(v[k], v[k + 1], 0x5410);
+            q.y = __byte_perm(v[k + 2], v[k + 3], 0x5410);
+            q.z = __byte_perm(v[k + 4], v[k + 5], 0x5410);
+            q.w = __byte_perm(v[k + 6], v[k + 7], 0x5410);
+            *reinterpret_cast<uint4 *>(rec + h * 32 + D6 * 8) = q;
+        } else {
+            *reinterpret_cast<int4 *>(rec + h * 32 + D6 * 8) = make_int4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+            *reinterpret_cast<int4 *>(rec + h * 32 + D6 * 8 + 4) = make_int4(v[k + 4], v[k + 5], v[k + 6], v[k + 7]);
+        }
+    }
+}
+
+__device__ __forceinline__ int staged_col_to_dlo(int col) {
+    const int D4 = ((col >> 5) << 1) | ((col >> 2) & 1), D6 = (col >> 3) & 3, D5 = col & 3;
+    return D4 * 16 + D5 * 4 + D6;
+}
+
+// Sub-tile s of this CTA -> tile, top setting digit r1, top outcome bit b1
+struct SubTile {
+    int64_t aH, c;
+    int r1, b1;
+};
+template <int Q>
+__device__ __forceinline__ SubTile subtile_of(const P1Args &a, int s) {
+    constexpr int SUB = Q == 7 ? 6 : 1;
+    const int64_t t = blockIdx.x + (int64_t)(s / SUB) * gridDim.x;
+    const int sub = s % SUB;
+    SubTile st;
+    st.aH = a.aH0 + t / a.C;
+    st.c = t % a.C;
+    st.r1 = sub >> 1;
+    st.b1 = sub & 1;
+    return st;
+}
+
+// L2 of one sub-tile: staged column `col` -> Pauli values, combined over the
+// Q = 7 top qubit (r1, b1) in the thread's private smem slabs tmp / oi.
+template <int Q, bool SMALL>
+__device__ __forceinline__ void l2_subtile(const P1Args &a, const SubTile &st, const typename Stage<SMALL>::T *stage,
+                                           int col, int32_t *tmp, int32_t *oi) {
+    constexpr int STRIDE = Stage<SMALL>::STRIDE;
+    const int dlo = staged_col_to_dlo(col);
+    int32_t *out = reinterpret_cast<int32_t *>(a.f.out) +
+                   (((st.aH - a.out_aH0) * a.C + st.c) << (2 * Q)) + dlo;
+    const int r1 = st.r1, b1 = st.b1;
+    l2_transform<typename Stage<SMALL>::T, STRIDE>(stage + col, [&](int D3, const int32_t(&v)[16]) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            const int r = k * 4 + D3;  // core digits D1 D2 D3
+            if constexpr (Q == 6) {
+                out[r * 64] = v[k];
+            } else if (b1 == 0) {
+                tmp[r * 64 + col] = v[k];
+            } else {
+                const int32_t u = tmp[r * 64 + col];
+                const int32_t acc = (r1 == 0 ? 0 : oi[r * 64 + col]) + u + v[k];
+                if (r1 < 2) oi[r * 64 + col] = acc;
+                else out[r * 64] = acc;                    // top digit I
+                out[(r1 + 1) * 4096 + r * 64] = u - v[k];  // top digit X / Y / Z
+            }
+        }
+    });
+}
+
+// Pass-1 tile kernel, LDG variant: persistent, 2 CTAs x 9 warps per SM in
+// SMALL mode.  Per sub-tile s (one __syncthreads):
+//   warps 0-6  L1(s): thread = row block rb x column chunk g; the 27 x 8
+//              count block -> 3 qubits in registers -> staged (int16);
+//   warps 7-8  L2(s-1): thread = staged column; the 27 x 8 staged values ->
+//              3 more qubits -> 64 values stored as whole 128-byte lines.
+// L1 warps wait on HBM while L2 warps compute, and the two CTAs of an SM
+// interleave their phases.  LOGN > 0 makes the row length 2^LOGN a
+// compile-time constant so the 27 row loads of an item are [base + imm]
+// (the runtime form costs ~5 integer instructions of address math per load).
+template <int Q, bool SMALL, typename Tin, int LOGN>
 __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(const P1Args a) {
     using ST = Stage<SMALL>;
     using T = typename ST::T;
@@ -311,76 +392,191 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
     constexpr int SUB = Q == 7 ? 6 : 1;
     constexpr int64_t Q3 = Q == 7 ? 2187 : 729;
     extern __shared__ __align__(16) unsigned char smem[];
-    int32_t *tmp = reinterpret_cast<int32_t *>(smem + 2 * ST::BYTES);  // [64 res][64 t]
-    int32_t *oi = tmp + 64 * 64;                                        // [64 res][64 t]
+    int32_t *tmp = reinterpret_cast<int32_t *>(smem + 2 * ST::BYTES);  // [64 r][64 col]
+    int32_t *oi = tmp + 64 * 64;                                        // [64 r][64 col]
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int64_t ntiles = a.naH * a.C;
-    const int64_t my_tiles = (int64_t)blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int64_t S = my_tiles * SUB;
+    const int my_tiles = (int64_t)blockIdx.x < ntiles ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+    const int S = my_tiles * SUB;
     const Tin *counts = reinterpret_cast<const Tin *>(a.counts);
+    const int rowlen = LOGN > 0 ? (1 << LOGN) : (int)a.rowlen;
 
-    for (int64_t s = 0; s <= S; ++s) {
+    for (int s = 0; s <= S; ++s) {
         if (warp < P1_L1_WARPS) {
             if (s < S && tid < P1_ITEMS) {
-                const int64_t t = blockIdx.x + (s / SUB) * (int64_t)gridDim.x;
-                const int sub = (int)(s % SUB);
-                const int r1 = sub >> 1, b1 = sub & 1;
-                const int64_t aH = a.aH0 + t / a.C, c = t % a.C;
+                const SubTile st = subtile_of<Q>(a, s);
                 const int rb = tid >> 3, g = tid & 7;
-                const int64_t row = aH * Q3 + (Q == 7 ? r1 * 729 : 0) + rb * 27 - a.row_base;
-                const int64_t col = (c << Q) + (Q == 7 ? b1 * 64 : 0) + g * 8;
-                const Tin *base = counts + row * a.rowlen + col;
+                const int64_t row = st.aH * Q3 + (Q == 7 ? st.r1 * 729 : 0) + rb * 27 - a.row_base;
+                const int64_t col = (st.c << Q) + (Q == 7 ? st.b1 * 64 : 0) + g * 8;
+                const Tin *base = counts + row * (int64_t)rowlen + col;
                 T *rec = reinterpret_cast<T *>(smem + (s & 1) * ST::BYTES) + tid * STRIDE;
-                auto stage = [&](int D6, const int32_t(&v)[16]) {
-                    if constexpr (SMALL) {
-#pragma unroll
-                        for (int k = 0; k < 16; k += 8) {
-                            uint4 q;
-                            q.x = __byte_perm(v[k], v[k + 1], 0x5410);
-                            q.y = __byte_perm(v[k + 2], v[k + 3], 0x5410);
-                            q.z = __byte_perm(v[k + 4], v[k + 5], 0x5410);
-                            q.w = __byte_perm(v[k + 6], v[k + 7], 0x5410);
-                            *reinterpret_cast<uint4 *>(rec + D6 * 16 + k) = q;
-                        }
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 16; k += 4)
-                            *reinterpret_cast<int4 *>(rec + D6 * 16 + k) = make_int4(v[k], v[k + 1], v[k + 2], v[k + 3]);
-                    }
-                };
-                if constexpr (SMALL) l1_small<Tin>(base, (int)a.rowlen, stage);
-                else l1_wide<Tin>(base, (int)a.rowlen, stage);
+                auto sink = [&](int D6, const int32_t(&v)[16]) { stage_record<SMALL>(rec, D6, v); };
+                if constexpr (SMALL) {
+                    l1_small([&](int j, uint32_t(&w)[4]) { load_packed(base + j * rowlen, w); }, sink);
+                } else {
+                    l1_wide([&](int j, int32_t(&w)[8]) { load_wide(base + j * rowlen, w); }, sink);
+                }
             }
         } else if (s > 0) {
-            const int64_t sp = s - 1;
-            const int64_t t = blockIdx.x + (sp / SUB) * (int64_t)gridDim.x;
-            const int sub = (int)(sp % SUB);
-            const int r1 = sub >> 1, b1 = sub & 1;
-            const int col = tid - 32 * P1_L1_WARPS;  // staged column 0..63
-            const int dlo = ((col & 15) << 2) | (col >> 4);
-            const int64_t tile_out = (a.aH0 + t / a.C - a.out_aH0) * a.C + t % a.C;
-            l2_transform<T, STRIDE>(reinterpret_cast<const T *>(smem + (sp & 1) * ST::BYTES) + col, [&](int D3, const int32_t(&v)[16]) {
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const int r = k * 4 + D3;  // core digits D1 D2 D3
-                    if constexpr (Q == 6) {
-                        p1_emit<Q>(a, tile_out, r * 64 + dlo, v[k]);
-                    } else if (b1 == 0) {
-                        tmp[r * 64 + col] = v[k];
-                    } else {
-                        const int32_t u = tmp[r * 64 + col];
-                        const int32_t sum = u + v[k];
-                        const int32_t acc = r1 == 0 ? sum : oi[r * 64 + col] + sum;
-                        if (r1 < 2) oi[r * 64 + col] = acc;
-                        else p1_emit<Q>(a, tile_out, r * 64 + dlo, acc);  // top digit I
-                        p1_emit<Q>(a, tile_out, (r1 + 1) * 4096 + r * 64 + dlo, u - v[k]);
-                    }
-                }
-            });
+            l2_subtile<Q, SMALL>(a, subtile_of<Q>(a, s - 1),
+                                 reinterpret_cast<const T *>(smem + ((s - 1) & 1) * ST::BYTES),
+                                 tid - 32 * P1_L1_WARPS, tmp, oi);
         }
         __syncthreads();
+    }
+}
+
+// ===========================================================================
+// pass 1, TMA variant (uint16 counts, SMALL mode): a producer warp streams
+// the 27-row x 128-byte box of every L1 row block into a ring of shared
+// memory slots with cp.async.bulk.tensor (128-byte swizzle, so the eight
+// 16-byte chunks of a row land in distinct banks for any row), completing on
+// mbarriers; L1 threads read their rows from shared memory.  Slot rb holds
+// row block rb of consecutive sub-tiles, so its fill number is the sub-tile
+// index and every waiter is at most one mbarrier phase ahead (a waiter two
+// phases ahead would alias parities: with fewer slots than row blocks, row
+// blocks rb and rb + NSLOT of one sub-tile raced and hung).  The ring keeps up
+// to one sub-tile (~93 KB) per SM in flight independent of L1/L2 compute.
+// ===========================================================================
+constexpr int TMA_NSLOT = 27;  // one slot per L1 row block: slot = rb, fill = sub-tile
+constexpr int TMA_SLOT_BYTES = 4096;  // 27 * 128 B, padded to the 1024-byte swizzle atom
+constexpr int TMA_BOX_BYTES = 27 * 128;
+constexpr int TMA_L1_WARPS = 7, TMA_L2_WARPS = 2;
+constexpr int TMA_COMPUTE_THREADS = 32 * (TMA_L1_WARPS + TMA_L2_WARPS);
+constexpr int TMA_THREADS = TMA_COMPUTE_THREADS + 32;  // + producer warp
+
+template <int Q> struct TmaSmem {
+    static constexpr size_t RING = (size_t)TMA_NSLOT * TMA_SLOT_BYTES;
+    static constexpr size_t STAGE = Stage<true>::BYTES;
+    static constexpr size_t EXTRA = P1Smem<Q, true>::EXTRA;
+    static constexpr size_t BARS = 2 * TMA_NSLOT * sizeof(uint64_t);
+    static constexpr size_t TOTAL = 1024 /* alignment slack */ + RING + 2 * STAGE + EXTRA + BARS;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef LRE_MBAR_WATCHDOG
+    // debug builds: trap (instead of hanging) when a phase never completes
+    for (long long it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == (1ll << 22)) {
+            if ((threadIdx.x & 31) == 0 || threadIdx.x >= TMA_COMPUTE_THREADS)
+                printf("LRE mbarrier watchdog: block %d thread %d bar %p parity %u\n", blockIdx.x, threadIdx.x, bar,
+                       parity);
+            __trap();
+        }
+    }
+#endif
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LRE_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra LRE_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int Q>
+__global__ void __launch_bounds__(TMA_THREADS, 1) tile_tma_kernel(const P1Args a, const __grid_constant__ CUtensorMap map) {
+    using ST = Stage<true>;
+    using T = ST::T;
+    constexpr int STRIDE = ST::STRIDE;
+    constexpr int SUB = Q == 7 ? 6 : 1;
+    constexpr int64_t Q3 = Q == 7 ? 2187 : 729;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *ring = smem;
+    unsigned char *stage0 = ring + TmaSmem<Q>::RING;
+    int32_t *tmp = reinterpret_cast<int32_t *>(stage0 + 2 * ST::BYTES);
+    int32_t *oi = tmp + 64 * 64;
+    uint64_t *full = reinterpret_cast<uint64_t *>(stage0 + 2 * ST::BYTES + TmaSmem<Q>::EXTRA);
+    uint64_t *empty = full + TMA_NSLOT;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int64_t ntiles = a.naH * a.C;
+    const int my_tiles = (int64_t)blockIdx.x < ntiles ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+    const int S = my_tiles * SUB;
+
+    if (tid == 0) {
+        for (int i = 0; i < TMA_NSLOT; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 8);  // the 8 L1 threads (column chunks) of a row block
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == TMA_L1_WARPS + TMA_L2_WARPS) {  // producer
+        if ((tid & 31) == 0) {
+            const int total = S * 27;
+            auto coords = [&](int q, int &col, int &row) {
+                const SubTile st = subtile_of<Q>(a, q / 27);
+                row = (int)(st.aH * Q3 + (Q == 7 ? st.r1 * 729 : 0) + (q % 27) * 27 - a.row_base);
+                col = (int)((st.c << Q) + (Q == 7 ? st.b1 * 64 : 0));
+            };
+            for (int q = 0; q < total; ++q) {
+                const int slot = q % TMA_NSLOT;  // == rb
+                int col, row;
+                if (q >= TMA_NSLOT) mbar_wait(&empty[slot], ((q / TMA_NSLOT) - 1) & 1);
+                coords(q, col, row);
+                mbar_expect_tx(&full[slot], TMA_BOX_BYTES);
+                tma_load_2d(ring + slot * TMA_SLOT_BYTES, &map, col, row, &full[slot]);
+            }
+        }
+        return;
+    }
+
+    for (int s = 0; s <= S; ++s) {
+        if (warp < TMA_L1_WARPS) {
+            if (s < S && tid < P1_ITEMS) {
+                const int rb = tid >> 3, g = tid & 7;
+                const int q = s * 27 + rb;
+                const int slot = q % TMA_NSLOT;
+                mbar_wait(&full[slot], (q / TMA_NSLOT) & 1);
+                const unsigned char *box = ring + slot * TMA_SLOT_BYTES;
+                T *rec = reinterpret_cast<T *>(stage0 + (s & 1) * ST::BYTES) + tid * STRIDE;
+                l1_small(
+                    [&](int j, uint32_t(&w)[4]) {
+                        const uint4 u = *reinterpret_cast<const uint4 *>(box + j * 128 + ((g ^ (j & 7)) << 4));
+                        w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
+                    },
+                    [&](int D6, const int32_t(&v)[16]) { stage_record<true>(rec, D6, v); });
+                mbar_arrive(&empty[slot]);
+            }
+        } else if (s > 0) {
+            l2_subtile<Q, true>(a, subtile_of<Q>(a, s - 1),
+                                reinterpret_cast<const T *>(stage0 + ((s - 1) & 1) * ST::BYTES),
+                                tid - 32 * TMA_L1_WARPS, tmp, oi);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(TMA_COMPUTE_THREADS) : "memory");
     }
 }
 
@@ -601,8 +797,12 @@ Plan make_plan(int n, int64_t shots, int dtype, int64_t w_begin, int64_t w_end) 
 static int g_num_sms = 0;
 static bool g_pow3_ready = false;
 
+static bool g_disable_tma;
+
 static cudaError_t ensure_init() {
     if (!g_pow3_ready) {
+        const char *env = getenv("LRE_P1_TMA");
+        g_disable_tma = !(env && env[0] == '1');
         double t[33];
         t[0] = 1.0;
         for (int i = 1; i < 33; ++i) t[i] = t[i - 1] * 3.0;
@@ -619,31 +819,95 @@ static cudaError_t ensure_init() {
     return cudaSuccess;
 }
 
-template <int Q, bool SMALL, typename Tin>
+template <int Q, bool SMALL, typename Tin, int LOGN = 0>
 static cudaError_t launch_tile(const P1Args &a, cudaStream_t s) {
-    auto kern = tile_pass_kernel<Q, SMALL, Tin>;
+    auto kern = tile_pass_kernel<Q, SMALL, Tin, LOGN>;
     const size_t smem = P1Smem<Q, SMALL>::TOTAL;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = a.naH * a.C;
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * (SMALL ? 2 : 1));
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * (SMALL ? 2 : 1));  // persistent
     kern<<<(unsigned)grid, P1_THREADS, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
+}
+
+// uint16 SMALL tiles (the benchmark format) get a compile-time row length
+template <int Q>
+static cudaError_t tile_u16_small(const P1Args &a, cudaStream_t s) {
+    switch (a.rowlen) {
+    case 1 << 7: return launch_tile<Q, true, uint16_t, 7>(a, s);
+    case 1 << 8: return launch_tile<Q, true, uint16_t, 8>(a, s);
+    case 1 << 9: return launch_tile<Q, true, uint16_t, 9>(a, s);
+    case 1 << 10: return launch_tile<Q, true, uint16_t, 10>(a, s);
+    case 1 << 11: return launch_tile<Q, true, uint16_t, 11>(a, s);
+    case 1 << 12: return launch_tile<Q, true, uint16_t, 12>(a, s);
+    case 1 << 13: return launch_tile<Q, true, uint16_t, 13>(a, s);
+    case 1 << 14: return launch_tile<Q, true, uint16_t, 14>(a, s);
+    default: return launch_tile<Q, true, uint16_t>(a, s);
+    }
 }
 
 template <int Q, bool SMALL>
 static cudaError_t tile_dtype(int dtype, const P1Args &a, cudaStream_t s) {
     switch (dtype) {
     case LRE_U8: return launch_tile<Q, SMALL, uint8_t>(a, s);
-    case LRE_U16: return launch_tile<Q, SMALL, uint16_t>(a, s);
+    case LRE_U16:
+        if constexpr (SMALL && Q == 7) return tile_u16_small<Q>(a, s);
+        return launch_tile<Q, SMALL, uint16_t>(a, s);
     case LRE_I32: return launch_tile<Q, SMALL, int32_t>(a, s);
     case LRE_I64: return launch_tile<Q, SMALL, int64_t>(a, s);
     default: return cudaErrorInvalidValue;
     }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static cudaError_t encode_counts_map(CUtensorMap *map, const P1Args &a, int Q) {
+    if (!g_encode) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr);
+        if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const int64_t q3 = ipow(3, Q);
+    const int64_t rows = (a.aH0 + a.naH) * q3 - a.row_base;  // rows held by the counts buffer
+    cuuint64_t dims[2] = {(cuuint64_t)a.rowlen, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)a.rowlen * sizeof(uint16_t)};
+    cuuint32_t box[2] = {64, 27};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<void *>(a.counts), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int Q>
+static cudaError_t launch_tma(const P1Args &a, cudaStream_t s) {
+    CUtensorMap map;
+    cudaError_t e = encode_counts_map(&map, a, Q);
+    if (e != cudaSuccess) return e;
+    auto kern = tile_tma_kernel<Q>;
+    const size_t smem = TmaSmem<Q>::TOTAL;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t ntiles = a.naH * a.C;
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms);
+    kern<<<(unsigned)grid, TMA_THREADS, smem, s>>>(a, map);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// pass 1 uses the LDG variant; LRE_P1_TMA=1 selects the TMA-ring variant (measured slower)
+
 static cudaError_t run_tile(int q, int small, int dtype, const P1Args &a, cudaStream_t s) {
+    if (small && dtype == LRE_U16 && !g_disable_tma && (a.rowlen * 2) % 16 == 0 &&
+        ((uintptr_t)a.counts & 15) == 0) {
+        if (q == 7) return launch_tma<7>(a, s);
+        if (q == 6) return launch_tma<6>(a, s);
+    }
 #ifdef LRE_ONLY_ONE
     return launch_tile<7, true, uint16_t>(a, s);
 #else
