@@ -1,17 +1,28 @@
-// Step (ii) of the LRE hot path on B200: theta (mask-major) -> mu (XOR-diagonals).
+// Step (ii) of the LRE hot path on B200: theta -> mu (XOR-diagonals).
 //
 // Reference: pipeline.py:93-101,141-161 (step_two_assemble) with
 // pauli.py:270-297 (omega_gather_indices / omega_phase_factors).  For every
 // X/Y mask m the reference gathers v[a] = theta[(m,a)] * (-i)^popcount(a&m),
 // runs a complex WHT of length 2^n and writes mu[r, r^m].
 //
-// B200 design (DESIGN.md §5): with w[a] = theta[(m,a)] * (-1)^floor(pc(a&m)/2)
+// B200 design (DESIGN.md §4): with w[a] = theta[(m,a)] * (-1)^floor(pc(a&m)/2)
 // and the real WHT F = H w, the complex WHT splits exactly as
 //     mu[r, r^m] = 2^{-n/2} ( (F[r] + F[r^m]) / 2  -  i (F[r] - F[r^m]) / 2 ),
-// so one real fp64 transform per mask replaces the complex one.  A CTA owns
-// MPC consecutive masks, keeps their transforms in shared memory (padded one
-// double per 16 to keep radix-16 rounds bank-conflict free) and writes MPC
-// adjacent complex columns per row, so rows of mu are written in runs.
+// so one real fp64 transform per mask replaces the complex one.
+//
+// A CTA owns a block of B consecutive masks (B = 2^j, the low j mask bits
+// vary), keeps their transforms in shared memory (radix-16 rounds, one pad
+// double per 16 so rounds are bank-conflict free) and
+//   * gathers theta in NATURAL order as runs of 4^j contiguous doubles (the
+//     low j qubits take all four Pauli digits across the block), and
+//   * writes each row r of mu as B adjacent complex values (the columns
+//     r ^ m of an aligned mask block are an aligned column block).
+// When one mask fills the shared memory (n >= 13: 2^14 doubles), two CTAs
+// form a cluster, each transforms one mask of an aligned pair, and the write
+// phase reads the partner's transform through distributed shared memory so
+// every row still gets a 32-byte pair.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cmath>
 
@@ -19,13 +30,15 @@
 
 namespace lre {
 
+namespace cg = cooperative_groups;
+
 __device__ __forceinline__ int padix(int i) { return i + (i >> 4); }
 
 template <int NB>
-__device__ __forceinline__ void wht_round(double *buf, int Dp, int logd, int mpc, int shift) {
+__device__ __forceinline__ void wht_round(double *buf, int Dp, int logd, int nm, int shift) {
     const int groups = (1 << logd) >> NB;
     const int lowmask = (1 << shift) - 1;
-    for (int it = threadIdx.x; it < mpc * groups; it += blockDim.x) {
+    for (int it = threadIdx.x; it < nm * groups; it += blockDim.x) {
         const int ml = it / groups, gi = it - ml * groups;
         const int base = (gi & lowmask) | ((gi >> shift) << (shift + NB));
         double *b = buf + ml * Dp;
@@ -46,67 +59,174 @@ __device__ __forceinline__ void wht_round(double *buf, int Dp, int logd, int mpc
     }
 }
 
-__global__ void __launch_bounds__(1024) assemble_kernel(const double *__restrict__ theta, int layout, int logd,
-                                                        int64_t m_begin, int64_t S, int mpc, double scale_half,
-                                                        double2 *__restrict__ mu) {
-    extern __shared__ double sbuf[];
-    const int d = 1 << logd;
-    const int Dp = d + (d >> 4) + 1;
-    const int64_t mloc0 = (int64_t)blockIdx.x * mpc;  // first mask of this CTA, relative to m_begin
-    // load + sign twist w[a] = theta[(m,a)] * (-1)^floor(popc(a&m)/2)
-    for (int e = threadIdx.x; e < mpc * d; e += blockDim.x) {
-        const int ml = e >> logd, a = e & (d - 1);
-        const uint32_t m = (uint32_t)(m_begin + mloc0 + ml);
-        // NATURAL: full theta, gathered at the natural index of (m, a); the CTA's
-        // consecutive masks cover all digits of the low qubits, so the gather
-        // reads whole lines.  MASK_MAJOR: the slice of masks [m_begin, m_end).
-        const int64_t idx = layout == LRE_LAYOUT_NATURAL ? (int64_t)ma_to_natural(m, (uint32_t)a)
-                                                         : (mloc0 + ml) * (int64_t)d + a;
-        double v = __ldg(theta + idx);
-        if ((__popc((uint32_t)a & m) >> 1) & 1) v = -v;
-        sbuf[ml * Dp + padix(a)] = v;
-    }
-    __syncthreads();
+__device__ __forceinline__ void wht_all(double *sbuf, int Dp, int logd, int nm) {
     int shift = 0;
     while (shift < logd) {
         const int nb = logd - shift >= 4 ? 4 : logd - shift;
         switch (nb) {
-        case 4: wht_round<4>(sbuf, Dp, logd, mpc, shift); break;
-        case 3: wht_round<3>(sbuf, Dp, logd, mpc, shift); break;
-        case 2: wht_round<2>(sbuf, Dp, logd, mpc, shift); break;
-        default: wht_round<1>(sbuf, Dp, logd, mpc, shift); break;
+        case 4: wht_round<4>(sbuf, Dp, logd, nm, shift); break;
+        case 3: wht_round<3>(sbuf, Dp, logd, nm, shift); break;
+        case 2: wht_round<2>(sbuf, Dp, logd, nm, shift); break;
+        default: wht_round<1>(sbuf, Dp, logd, nm, shift); break;
         }
         shift += nb;
         __syncthreads();
     }
-    // mu[r, r^m] for the CTA's masks; consecutive threads take consecutive
-    // masks of the same row so each row is written as an mpc-long run.
-    for (int e = threadIdx.x; e < mpc * d; e += blockDim.x) {
-        const int ml = e % mpc, r = e / mpc;
-        const uint32_t m = (uint32_t)(m_begin + mloc0 + ml);
-        const double *b = sbuf + ml * Dp;
-        const double f1 = b[padix(r)], f2 = b[padix(r ^ m)];
-        const int64_t col = (int64_t)((r ^ m) & (uint32_t)(S - 1));
-        __stcs(mu + (int64_t)r * S + col, make_double2(scale_half * (f1 + f2), scale_half * (f2 - f1)));
+}
+
+struct AsmArgs {
+    const double *theta;
+    int layout;      // LRE_LAYOUT_NATURAL (full theta) or MASK_MAJOR (slice of [m_begin, m_end))
+    int logd;        // n
+    int logb;        // j: B = 2^j masks per CTA
+    int cl;          // CTAs per cluster (1 or 2)
+    int64_t m_begin;
+    int64_t S;       // masks in the slice (power of two); mu rows are S complex wide
+    int64_t groups;  // mask groups of B * cl masks
+    double scale_half;
+    double2 *mu;
+};
+
+// load + sign twist of the CTA's B masks [mloc0, mloc0 + B) into shared memory
+__device__ __forceinline__ void asm_load(const AsmArgs &a, double *sbuf, int Dp, int64_t mloc0) {
+    const int d = 1 << a.logd;
+    const int B = 1 << a.logb;
+    if (a.layout == LRE_LAYOUT_NATURAL) {
+        // e = a_high * 4^j + d_low: consecutive threads read a contiguous run
+        // of 4^j natural indices (the low j qubits' digits).
+        const int j = a.logb;
+        const uint32_t mhigh = (uint32_t)((a.m_begin + mloc0) >> j);
+        for (int e = threadIdx.x; e < B * d; e += blockDim.x) {
+            const uint32_t dlow = (uint32_t)e & ((1u << (2 * j)) - 1);
+            const uint32_t ahigh = (uint32_t)e >> (2 * j);
+            // decode the low digits: digit X/Y -> mask bit, Y/Z -> a bit
+            const uint32_t hi = compact_odd(dlow), lo = compact_even(dlow);
+            const uint32_t alow = hi, mlow = hi ^ lo;
+            const uint32_t m = (mhigh << j) | mlow;
+            const uint32_t av = (ahigh << j) | alow;
+            const uint64_t nat = ma_to_natural(m, av);
+            double v = __ldg(a.theta + nat);
+            if ((__popc(av & m) >> 1) & 1) v = -v;
+            sbuf[mlow * Dp + padix((int)av)] = v;
+        }
+    } else {
+        for (int e = threadIdx.x; e < B * d; e += blockDim.x) {
+            const int ml = e >> a.logd, av = e & (d - 1);
+            const uint32_t m = (uint32_t)(a.m_begin + mloc0 + ml);
+            double v = __ldg(a.theta + (mloc0 + ml) * (int64_t)d + av);
+            if ((__popc((uint32_t)av & m) >> 1) & 1) v = -v;
+            sbuf[ml * Dp + padix(av)] = v;
+        }
     }
 }
 
-int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu,
-                  cudaStream_t s) {
+__global__ void __launch_bounds__(1024, 1) assemble_kernel(const AsmArgs a) {
+    extern __shared__ double sbuf[];
+    const int d = 1 << a.logd;
+    const int Dp = d + (d >> 4) + 1;
+    const int B = 1 << a.logb;
+    const int64_t S = a.S;
+    for (int64_t grp = blockIdx.x; grp < a.groups; grp += gridDim.x) {
+        const int64_t mloc0 = grp * B;  // relative to m_begin
+        asm_load(a, sbuf, Dp, mloc0);
+        __syncthreads();
+        wht_all(sbuf, Dp, a.logd, B);
+        // rows of mu as runs of B adjacent complex values
+        for (int e = threadIdx.x; e < B * d; e += blockDim.x) {
+            const int ml = e & (B - 1), r = e >> a.logb;
+            const uint32_t m = (uint32_t)(a.m_begin + mloc0 + ml);
+            const double *b = sbuf + ml * Dp;
+            const double f1 = b[padix(r)], f2 = b[padix(r ^ (int)m)];
+            const int64_t col = (int64_t)((r ^ m) & (uint32_t)(S - 1));
+            __stcs(a.mu + (int64_t)r * S + col, make_double2(a.scale_half * (f1 + f2), a.scale_half * (f2 - f1)));
+        }
+        __syncthreads();
+    }
+}
+
+// n >= 13: a cluster of two CTAs transforms the aligned mask pair (m0, m0 + 1);
+// CTA k writes rows [k d/2, (k+1) d/2) of both masks, reading the partner's
+// transform through distributed shared memory -> 32-byte row segments.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024, 1) assemble_pair_kernel(const AsmArgs a) {
+    extern __shared__ double sbuf[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int d = 1 << a.logd;
+    const int Dp = d + (d >> 4) + 1;
+    const int64_t S = a.S;
+    const double *own = sbuf;
+    const double *peer = cluster.map_shared_rank(sbuf, rank ^ 1);
+    const double *tr0 = rank == 0 ? own : peer;  // transform of mask m0
+    const double *tr1 = rank == 0 ? peer : own;  // transform of mask m0 + 1
+    const int64_t ncl = gridDim.x / 2;
+    for (int64_t grp = blockIdx.x / 2; grp < a.groups; grp += ncl) {
+        const int64_t mloc0 = grp * 2;
+        asm_load(a, sbuf, Dp, mloc0 + rank);
+        __syncthreads();
+        wht_all(sbuf, Dp, a.logd, 1);
+        cluster.sync();  // both transforms complete
+        const uint32_t m0 = (uint32_t)(a.m_begin + mloc0), m1 = m0 + 1;
+        for (int r = rank * (d >> 1) + threadIdx.x; r < (rank + 1) * (d >> 1); r += blockDim.x) {
+            const double f01 = tr0[padix(r)], f02 = tr0[padix(r ^ (int)m0)];
+            const double f11 = tr1[padix(r)], f12 = tr1[padix(r ^ (int)m1)];
+            const double2 v0 = make_double2(a.scale_half * (f01 + f02), a.scale_half * (f02 - f01));
+            const double2 v1 = make_double2(a.scale_half * (f11 + f12), a.scale_half * (f12 - f11));
+            const int64_t c0 = (int64_t)((r ^ m0) & (uint32_t)(S - 1));  // c0 ^ 1 is mask m1's column
+            double2 *dst = a.mu + (int64_t)r * S + (c0 & ~(int64_t)1);
+            if (c0 & 1) {
+                __stcs(dst, v1);
+                __stcs(dst + 1, v0);
+            } else {
+                __stcs(dst, v0);
+                __stcs(dst + 1, v1);
+            }
+        }
+        cluster.sync();  // the partner has finished reading this CTA's transform
+    }
+}
+
+int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s) {
     const int64_t S = m_end - m_begin;
     const int64_t d = (int64_t)1 << n;
     if (n < 1 || n > 14) return LRE_EUNSUPPORTED;
     if (S <= 0 || (S & (S - 1)) || m_begin % S || m_end > d) return LRE_EINVAL;
-    int mpc = 1;
-    while (mpc < 8 && (int64_t)mpc * 2 <= S && ((int64_t)mpc * 2 * d) <= (1 << 14)) mpc *= 2;
+    static int num_sms = 0;
+    if (!num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
     const int Dp = (int)(d + (d >> 4) + 1);
-    const size_t smem = (size_t)mpc * Dp * sizeof(double);
-    int threads = (int)std::min<int64_t>(1024, std::max<int64_t>(64, mpc * d / 16));
-    cudaError_t e = cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return LRE_ECUDA;
-    const double scale_half = 0.5 * pow(2.0, -n / 2.0);
-    assemble_kernel<<<(unsigned)(S / mpc), threads, smem, s>>>(theta, layout, n, m_begin, S, mpc, scale_half,
-                                                              reinterpret_cast<double2 *>(mu));
+    const size_t smem_budget = 150 * 1024;
+    int logb = 0;
+    while (logb < 3 && ((int64_t)2 << logb) <= S && (size_t)(2 << logb) * Dp * sizeof(double) <= smem_budget) ++logb;
+    AsmArgs a;
+    a.theta = theta;
+    a.layout = layout;
+    a.logd = n;
+    a.logb = logb;
+    a.m_begin = m_begin;
+    a.S = S;
+    a.scale_half = 0.5 * pow(2.0, -n / 2.0);
+    a.mu = reinterpret_cast<double2 *>(mu);
+    const size_t smem = ((size_t)Dp << logb) * sizeof(double);
+    const int threads = (int)std::min<int64_t>(1024, std::max<int64_t>(64, (d << logb) / 16));
+    cudaError_t e;
+    if (logb == 0 && S >= 2) {
+        a.cl = 2;
+        a.groups = S / 2;
+        e = cudaFuncSetAttribute(assemble_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return LRE_ECUDA;
+        const int64_t grid = 2 * std::min<int64_t>(a.groups, num_sms / 2);
+        assemble_pair_kernel<<<(unsigned)grid, threads, smem, s>>>(a);
+    } else {
+        a.cl = 1;
+        a.groups = S >> logb;
+        e = cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return LRE_ECUDA;
+        const int64_t grid = std::min<int64_t>(a.groups, (int64_t)num_sms * (smem <= 110 * 1024 ? 2 : 1));
+        assemble_kernel<<<(unsigned)grid, threads, smem, s>>>(a);
+    }
     count_launch();
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
 }

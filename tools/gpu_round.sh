@@ -29,4 +29,4 @@ if [ -n "$NCU_FULL_N" ]; then
     echo "ncu full $k rc=$?" >> $O/ncu_full_$k.log
   done
 fi
-tail -3 $O/smoke.log 2>/dev/null; tail -5 $O/pytest_gpu.log 2>/dev/null; cat $O/bench_n*.json; tail -3 $O/bench_n*.err
+tail -3 $O/smoke.log 2>/dev/null; tail -5 $O/pytest_gpu.log 2>/dev/null; cat $O/bench_n*.json; for f in $O/bench_n*.err; do tail -n 3 $f; done
