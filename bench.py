@@ -105,6 +105,20 @@ class ClockSampler:
 # CPU baseline: the reference algorithm's C port on bounded samples
 # ---------------------------------------------------------------------------
 
+def workload_name(args) -> str:
+    """BASELINE.json config C5 (n = 14; other n are the parity configs C1-C4 shapes)."""
+    return (f"C5: n={args.n} {args.state.upper()}, 3^{args.n} settings x 2^{args.n} outcomes, "
+            f"{args.shots} shots/setting, seed {args.seed}, one reconstruction (steps i+ii) per step")
+
+
+def baseline_settings(n: int) -> int:
+    """Settings in the bounded step-(i) sample (about 10-20 s of single-node CPU work at n = 14)."""
+    threads = os.cpu_count() or 1
+    d = 1 << n
+    S = max(threads * 4, min(3**n // 8, int(2e6 // d) * threads))
+    return min(S, 3**n // 2)
+
+
 def cpu_baseline(n: int, shots: int, seed: int, counts_rows=None, budget_s: float = 20.0):
     """Extrapolated seconds of the reference LRE (steps i+ii) on the host cores.
 
@@ -118,8 +132,7 @@ def cpu_baseline(n: int, shots: int, seed: int, counts_rows=None, budget_s: floa
 
     threads = os.cpu_count() or 1
     d = 1 << n
-    S = max(threads * 4, min(3**n // 8, int(2e6 // d) * threads))
-    S = min(S, 3**n // 2)
+    S = baseline_settings(n)
     rows = counts_rows if counts_rows is not None and counts_rows.shape[0] >= 2 * S else \
         O.sample_ghz_counts(n, shots, seed, 0, 2 * S)
     t = []
@@ -261,9 +274,7 @@ def run_b200(args):
 
     base = None
     if not args.no_cpu_baseline:
-        d = 1 << n
-        S = max((os.cpu_count() or 1) * 4, min(3**n // 8, int(2e6 // d) * (os.cpu_count() or 1)))
-        S = min(S, 3**n // 2)
+        S = baseline_settings(n)
         base = cpu_baseline(n, shots, seed, counts[: 2 * S].cpu().numpy())
 
     plan = lre.LREPlan(n, shots, dev)
@@ -354,9 +365,8 @@ def run_b200(args):
         "vs_baseline": t_step / PAPER_STEPS_12_S if n == 14 else None,
         "dtype": "i32/i64 exact integer folds, f64 theta/mu",
         "data": "synthetic: device generator, Philox4x32-10 per (seed, setting), multinomial shots",
-        "config": {"workload": f"C5: n={n} {args.state.upper()}, 3^{n} settings x 2^{n} outcomes, {shots} shots/setting, "
-                               f"seed {seed}, {ctype} counts resident in HBM",
-                   "n": n, "state": args.state, "shots": shots, "count_bytes": c,
+        "config": {"workload": workload_name(args), "n": n, "state": args.state, "shots": shots,
+                   "counts": f"{ctype}, resident in HBM", "count_bytes": c,
                    "l2": "inputs larger than L2 (counts >> 126 MB); no flush",
                    "passes": plan.passes,
                    "vs_baseline_ref": "paper GTX 780 steps (i)+(ii) at n=14, 2.86 h (PAPER.md:167,169)"},
@@ -396,20 +406,27 @@ def run_reference(args):
     n, shots, seed = args.n, args.shots, args.seed
     from oracle import c_oracle as C
 
+    from oracle import lre_oracle as O
+
     C.build()
+    # one bounded sample of the workload per step; the counts sample is drawn
+    # once, and at most 6 steps are timed so the arm ends within minutes for
+    # any --steps (the median is reported; `steps` says how many were timed)
+    rows = O.sample_ghz_counts(n, shots, seed, 0, 2 * baseline_settings(n))
+    warm, timed = min(1, max(0, args.warmup)), max(1, min(args.steps, 6))
     vals = []
     last = None
-    for i in range(max(1, args.warmup) + max(1, args.steps)):
-        last = cpu_baseline(n, shots, seed, None)
-        if i >= max(1, args.warmup):
+    for i in range(warm + timed):
+        last = cpu_baseline(n, shots, seed, rows)
+        if i >= warm:
             vals.append(last["value"])
     v = statistics.median(vals)
     line = {
         "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": len(vals), "warmup": args.warmup,
         "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic: GHZ multinomial counts (numpy Philox per setting, simulate.py:216-242)",
-        "config": {"workload": f"C5: n={n} {args.state.upper()}, 3^{n} settings x 2^{n} outcomes, {shots} shots/setting",
-                   "n": n, "state": args.state, "shots": shots},
+        "config": {"workload": workload_name(args), "n": n, "state": args.state, "shots": shots,
+                   "counts": "host-resident sample, see cpu_baseline.sample"},
         "impl": "reference",
         "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": v},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

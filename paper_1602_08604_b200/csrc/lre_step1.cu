@@ -707,6 +707,67 @@ __global__ void __launch_bounds__(128, 4) vfold_kernel(const VArgs a) {
     }
 }
 
+// vfold3: three qubits per pass for int32 data with V >= 32.  Each warp owns
+// one task = (A, B, 32 consecutive v): it stages the task's 27 x 8 input
+// lines (27 KB) in shared memory with coalesced 16-byte loads (54 per lane,
+// 18 in flight), then every lane runs the 3-qubit transform on its v at
+// compile-time shared-memory offsets and writes 64 whole 128-byte lines.
+// The register-only vfold needs 216 runtime-strided 64-bit addresses per
+// thread for Q = 3, which does not fit; Q = 3 cuts the n = 14 step-(i)
+// traffic from 223 GB (7+2+2+2+1) to 210 GB (7+3+3+1).
+constexpr int VF3_WARPS = 4;
+constexpr int VF3_TASK_INTS = 216 * 32;
+
+template <bool FINAL>
+__global__ void __launch_bounds__(32 * VF3_WARPS, 2) vfold3_kernel(const VArgs a) {
+    extern __shared__ __align__(16) int32_t vsm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int32_t *st = vsm + warp * VF3_TASK_INTS;
+    const int64_t V = a.V;
+    const int64_t nvb = V >> 5;
+    const int64_t ntask = a.nA * a.nB * nvb;
+    const int32_t *in = reinterpret_cast<const int32_t *>(a.in);
+    const int64_t rstride = a.ncol * V;
+    for (int64_t t = (int64_t)blockIdx.x * VF3_WARPS + warp; t < ntask; t += (int64_t)gridDim.x * VF3_WARPS) {
+        const int64_t vb = t % nvb;
+        const int64_t rest = t / nvb;
+        const int64_t B = rest % a.nB;
+        const int64_t A = a.A0 + rest / a.nB;
+        const int64_t v0 = vb << 5;
+        const int64_t row0 = A * 27;
+        const int32_t *p0 = in + ((row0 - a.xa0) * a.ncol + B * 8) * V + v0;
+        // chunk id = lane + 32 k: line L = id >> 3 (= j*8 + s), 16-byte chunk c = id & 7
+#pragma unroll
+        for (int k0 = 0; k0 < 54; k0 += 18) {
+            int4 q[18];
+#pragma unroll
+            for (int k = 0; k < 18; ++k) {
+                const int id = lane + 32 * (k0 + k);
+                const int L = id >> 3, c = id & 7, j = L >> 3, s = L & 7;
+                const int64_t row = row0 + j;
+                q[k] = (row >= a.alo && row < a.ahi)
+                           ? __ldcs(reinterpret_cast<const int4 *>(p0 + j * rstride + s * V) + c)
+                           : make_int4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < 18; ++k) {
+                const int id = lane + 32 * (k0 + k);
+                reinterpret_cast<int4 *>(st)[id] = q[k];
+            }
+        }
+        __syncwarp();
+        auto ld = [&](int r1, int j, int s) -> int32_t { return st[((r1 * 9 + j) * 8 + s) * 32 + lane]; };
+        const int64_t v = v0 + lane;
+        if constexpr (!FINAL) {
+            int32_t *out = reinterpret_cast<int32_t *>(a.f.out) + ((A - a.ya0) * a.nB + B) * 64 * V + v;
+            vblock<3, int32_t>(ld, [&](int d, int32_t y) { out[(int64_t)d * V] = y; });
+        } else {
+            vblock<3, int32_t>(ld, [&](int d, int32_t y) { store_final(a.f, (uint64_t)(d * V + v), (int64_t)y); });
+        }
+        __syncwarp();
+    }
+}
+
 // ===========================================================================
 // host-side planning
 // ===========================================================================
@@ -759,10 +820,14 @@ Plan make_plan(int n, int64_t shots, int dtype, int64_t w_begin, int64_t w_end) 
     std::vector<int> qs;
     qs.push_back(q1);
     int rem = n - q1;
+    int done_q = q1;
     while (rem > 0) {
-        const int q = std::min(VFOLD_MAX_Q, rem);
+        // shared-memory staged Q = 3 passes need int32 data and V = 4^done >= 32
+        const bool q3 = done_q >= 3 && fits_i32(shots, done_q + 3);
+        const int q = std::min(q3 ? 3 : VFOLD_MAX_Q, rem);
         qs.push_back(q);
         rem -= q;
+        done_q += q;
     }
     for (size_t i = 0; i < qs.size(); ++i) {
         Pass ps{};
@@ -771,7 +836,7 @@ Plan make_plan(int n, int64_t shots, int dtype, int64_t w_begin, int64_t w_end) 
         ps.small = (ps.kind == 0 && shots <= SMALL_MAX_SHOTS) ? 1 : 0;
         ps.in_dtype = i == 0 ? dtype : (pl.p[i - 1].acc64 ? LRE_I64 : LRE_I32);
         const bool last = i + 1 == qs.size();
-        ps.acc64 = (ps.kind == 1 && (last || !fits_i32(shots, done + ps.q))) ? 1 : 0;
+        ps.acc64 = (ps.kind == 1 && !fits_i32(shots, done + ps.q)) ? 1 : 0;
         ps.alo = lo;
         ps.ahi = hi;
         const int64_t q3 = ipow(3, ps.q);
@@ -926,11 +991,35 @@ static cudaError_t launch_vfold(const VArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+static cudaError_t launch_vfold3(const VArgs &a, cudaStream_t s) {
+    const size_t smem = (size_t)VF3_WARPS * VF3_TASK_INTS * sizeof(int32_t);
+    const int64_t tasks = a.nA * a.nB * (a.V >> 5);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + VF3_WARPS - 1) / VF3_WARPS,
+                                                                (int64_t)g_num_sms * 2));
+    cudaError_t e;
+    if (a.f.kind == OUT_INTER) {
+        e = cudaFuncSetAttribute(vfold3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        vfold3_kernel<false><<<(unsigned)grid, 32 * VF3_WARPS, smem, s>>>(a);
+    } else {
+        e = cudaFuncSetAttribute(vfold3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        vfold3_kernel<true><<<(unsigned)grid, 32 * VF3_WARPS, smem, s>>>(a);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
 template <typename Tin, typename Ta>
 static cudaError_t vfold_q(int q, const VArgs &a, cudaStream_t s) {
     switch (q) {
     case 1: return launch_vfold<1, Tin, Ta>(a, s);
     case 2: return launch_vfold<2, Tin, Ta>(a, s);
+    case 3:
+        if constexpr (sizeof(Tin) == 4 && sizeof(Ta) == 4) {
+            if (a.V >= 32) return launch_vfold3(a, s);
+        }
+        return cudaErrorInvalidValue;
     default: return cudaErrorInvalidValue;
     }
 }

@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(1024, 1) assemble_kernel(const AsmArgs a) {
 // n >= 13: a cluster of two CTAs transforms the aligned mask pair (m0, m0 + 1);
 // CTA k writes rows [k d/2, (k+1) d/2) of both masks, reading the partner's
 // transform through distributed shared memory -> 32-byte row segments.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024, 1) assemble_pair_kernel(const AsmArgs a) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) assemble_pair_kernel(const AsmArgs a) {
     extern __shared__ double sbuf[];
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
@@ -159,13 +159,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(1024, 1) assemble_pa
     const double *tr0 = rank == 0 ? own : peer;  // transform of mask m0
     const double *tr1 = rank == 0 ? peer : own;  // transform of mask m0 + 1
     const int64_t ncl = gridDim.x / 2;
+    double *dst0 = rank == 0 ? sbuf : cluster.map_shared_rank(sbuf, 0);  // mask m0's buffer
+    double *dst1 = rank == 1 ? sbuf : cluster.map_shared_rank(sbuf, 1);  // mask m0 + 1's buffer
     for (int64_t grp = blockIdx.x / 2; grp < a.groups; grp += ncl) {
         const int64_t mloc0 = grp * 2;
-        asm_load(a, sbuf, Dp, mloc0 + rank);
-        __syncthreads();
+        const uint32_t m0 = (uint32_t)(a.m_begin + mloc0);
+        if (a.layout == LRE_LAYOUT_NATURAL) {
+            // Natural theta of the pair comes in 32-byte runs (the lowest qubit's
+            // I, X, Y, Z): I/Z belong to m0 (a_low = 0/1), X/Y to m0 + 1.  CTA k
+            // loads the runs of half of the a_high values (8 runs in flight per
+            // thread) and stores into both masks' buffers (one via DSMEM).
+            const uint32_t mh = m0 >> 1;
+            const int half = d >> 2;  // a_high values per CTA
+            constexpr int U = 4;
+            for (int base = threadIdx.x; base < half; base += U * blockDim.x) {
+                double4 q[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int ah = rank * half + base + u * blockDim.x;
+                    if (base + u * (int)blockDim.x < half) {
+                        const uint64_t run = ma_to_natural(mh, (uint32_t)ah);  // natural index / 4
+                        const double2 *p = reinterpret_cast<const double2 *>(a.theta + 4 * run);
+                        const double2 lo = __ldg(p), hi = __ldg(p + 1);
+                        q[u] = make_double4(lo.x, lo.y, hi.x, hi.y);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int ah = rank * half + base + u * blockDim.x;
+                    if (base + u * (int)blockDim.x < half) {
+                        const uint32_t a0 = (uint32_t)ah << 1, a1 = a0 | 1u;
+                        const uint32_t m1 = m0 + 1;
+                        // I: (m0, a0), Z: (m0, a1), X: (m1, a0), Y: (m1, a1)
+                        const double vI = ((__popc(a0 & m0) >> 1) & 1) ? -q[u].x : q[u].x;
+                        const double vZ = ((__popc(a1 & m0) >> 1) & 1) ? -q[u].w : q[u].w;
+                        const double vX = ((__popc(a0 & m1) >> 1) & 1) ? -q[u].y : q[u].y;
+                        const double vY = ((__popc(a1 & m1) >> 1) & 1) ? -q[u].z : q[u].z;
+                        dst0[padix((int)a0)] = vI;
+                        dst0[padix((int)a1)] = vZ;
+                        dst1[padix((int)a0)] = vX;
+                        dst1[padix((int)a1)] = vY;
+                    }
+                }
+            }
+            cluster.sync();  // both buffers filled (local and remote stores)
+        } else {
+            asm_load(a, sbuf, Dp, mloc0 + rank);
+            __syncthreads();
+        }
         wht_all(sbuf, Dp, a.logd, 1);
         cluster.sync();  // both transforms complete
-        const uint32_t m0 = (uint32_t)(a.m_begin + mloc0), m1 = m0 + 1;
+        const uint32_t m1 = m0 + 1;
         for (int r = rank * (d >> 1) + threadIdx.x; r < (rank + 1) * (d >> 1); r += blockDim.x) {
             const double f01 = tr0[padix(r)], f02 = tr0[padix(r ^ (int)m0)];
             const double f11 = tr1[padix(r)], f12 = tr1[padix(r ^ (int)m1)];
@@ -218,7 +262,7 @@ int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64
         e = cudaFuncSetAttribute(assemble_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return LRE_ECUDA;
         const int64_t grid = 2 * std::min<int64_t>(a.groups, num_sms / 2);
-        assemble_pair_kernel<<<(unsigned)grid, threads, smem, s>>>(a);
+        assemble_pair_kernel<<<(unsigned)grid, 512, smem, s>>>(a);
     } else {
         a.cl = 1;
         a.groups = S >> logb;

@@ -45,15 +45,16 @@ def test_host_only_entry_points():
     assert lib.lre_strerror(_lib.LRE_EINVAL) == b"invalid argument"
     assert lib.lre_shard_quantum(14) == 3**7
     assert lib.lre_shard_quantum(5) == 3**5
-    assert lib.lre_step1_num_passes(14, 1000) == 5      # tile pass (7) + 2 + 2 + 2 + 1
-    assert lib.lre_step1_num_passes(12, 1000) == 4      # 7 + 2 + 2 + 1
-    assert lib.lre_step1_num_passes(4, 16) == 2         # 2 + 2 (vector passes only)
+    assert lib.lre_step1_num_passes(14, 1000) == 4      # tile pass (7) + 3 + 3 + 1
+    assert lib.lre_step1_num_passes(12, 1000) == 3      # 7 + 3 + 2
+    assert lib.lre_step1_num_passes(4, 16) == 2         # 2 + 2 (vector passes from raw counts)
+    assert lib.lre_step1_num_passes(14, 3_000_000_000) == 7  # int64 plan: 2-qubit passes
     import ctypes
 
     ws = ctypes.c_size_t(0)
     assert lib.lre_step1_workspace(14, 1000, 0, 3**14, ctypes.byref(ws)) == _lib.LRE_OK
     y1 = 4**7 * 3**7 * 2**7 * 4
-    y2 = 4**9 * 3**5 * 2**5 * 4
+    y2 = 4**10 * 3**4 * 2**4 * 4
     assert ws.value >= y1 + y2 and ws.value < y1 + y2 + 4096
 
 
