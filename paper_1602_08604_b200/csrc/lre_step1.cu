@@ -708,64 +708,120 @@ __global__ void __launch_bounds__(128, 4) vfold_kernel(const VArgs a) {
 }
 
 // vfold3: three qubits per pass for int32 data with V >= 32.  Each warp owns
-// one task = (A, B, 32 consecutive v): it stages the task's 27 x 8 input
-// lines (27 KB) in shared memory with coalesced 16-byte loads (54 per lane,
-// 18 in flight), then every lane runs the 3-qubit transform on its v at
-// compile-time shared-memory offsets and writes 64 whole 128-byte lines.
-// The register-only vfold needs 216 runtime-strided 64-bit addresses per
-// thread for Q = 3, which does not fit; Q = 3 cuts the n = 14 step-(i)
-// traffic from 223 GB (7+2+2+2+1) to 210 GB (7+3+3+1).
+// tasks = (A, B, 32 consecutive v); a task's 27 x 8 input lines are 128-byte
+// lines (one per lane-wide v block).  The transform streams over the top row
+// digit r1, so the lines arrive as three groups of 9 rows x 8 columns (9 KB)
+// through a per-warp ring of three cp.async slots: while group q computes,
+// groups q+1 and q+2 are in flight, with no registers held for them.  Every
+// lane then runs the r1 step on its v at compile-time shared-memory offsets
+// and writes whole 128-byte lines.  (Q = 3 cuts the n = 14 step-(i) traffic
+// from 223 GB (7+2+2+2+1) to 210 GB (7+3+3+1); the register-only vfold
+// would need 216 runtime-strided 64-bit addresses per thread.)
 constexpr int VF3_WARPS = 4;
-constexpr int VF3_TASK_INTS = 216 * 32;
+constexpr int VF3_GROUP_CHUNKS = 72 * 8;  // 16-byte chunks per r1 group (72 lines x 128 B)
+constexpr int VF3_SLOTS = 3;
+
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc), "r"(src_bytes)
+                 : "memory");
+}
 
 template <bool FINAL>
 __global__ void __launch_bounds__(32 * VF3_WARPS, 2) vfold3_kernel(const VArgs a) {
-    extern __shared__ __align__(16) int32_t vsm[];
+    extern __shared__ __align__(16) int4 vsm4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int32_t *st = vsm + warp * VF3_TASK_INTS;
+    int4 *ring = vsm4 + warp * VF3_SLOTS * VF3_GROUP_CHUNKS;
     const int64_t V = a.V;
     const int64_t nvb = V >> 5;
     const int64_t ntask = a.nA * a.nB * nvb;
     const int32_t *in = reinterpret_cast<const int32_t *>(a.in);
-    const int64_t rstride = a.ncol * V;
-    for (int64_t t = (int64_t)blockIdx.x * VF3_WARPS + warp; t < ntask; t += (int64_t)gridDim.x * VF3_WARPS) {
-        const int64_t vb = t % nvb;
+    const int64_t gw = (int64_t)blockIdx.x * VF3_WARPS + warp, nw = (int64_t)gridDim.x * VF3_WARPS;
+    const int my_tasks = gw < ntask ? (int)((ntask - 1 - gw) / nw) + 1 : 0;
+    const int nq = my_tasks * 3;
+
+    auto task_coords = [&](int i, int64_t &A, int64_t &B, int64_t &v0) {
+        const int64_t t = gw + (int64_t)i * nw;
+        v0 = (t % nvb) << 5;
         const int64_t rest = t / nvb;
-        const int64_t B = rest % a.nB;
-        const int64_t A = a.A0 + rest / a.nB;
-        const int64_t v0 = vb << 5;
-        const int64_t row0 = A * 27;
-        const int32_t *p0 = in + ((row0 - a.xa0) * a.ncol + B * 8) * V + v0;
-        // chunk id = lane + 32 k: line L = id >> 3 (= j*8 + s), 16-byte chunk c = id & 7
-#pragma unroll
-        for (int k0 = 0; k0 < 54; k0 += 18) {
-            int4 q[18];
+        B = rest % a.nB;
+        A = a.A0 + rest / a.nB;
+    };
+    auto issue = [&](int q) {
+        if (q < nq) {
+            int64_t A, B, v0;
+            task_coords(q / 3, A, B, v0);
+            const int r1 = q % 3;
+            const int64_t row0 = A * 27 + r1 * 9;
+            const int32_t *p0 = in + ((row0 - a.xa0) * a.ncol + B * 8) * V + v0;
+            int4 *slot = ring + (q % VF3_SLOTS) * VF3_GROUP_CHUNKS;
 #pragma unroll
             for (int k = 0; k < 18; ++k) {
-                const int id = lane + 32 * (k0 + k);
+                const int id = lane + 32 * k;
                 const int L = id >> 3, c = id & 7, j = L >> 3, s = L & 7;
                 const int64_t row = row0 + j;
-                q[k] = (row >= a.alo && row < a.ahi)
-                           ? __ldcs(reinterpret_cast<const int4 *>(p0 + j * rstride + s * V) + c)
-                           : make_int4(0, 0, 0, 0);
-            }
-#pragma unroll
-            for (int k = 0; k < 18; ++k) {
-                const int id = lane + 32 * (k0 + k);
-                reinterpret_cast<int4 *>(st)[id] = q[k];
+                const bool ok = row >= a.alo && row < a.ahi;
+                cp_async16(slot + id, ok ? (const void *)(p0 + (j * a.ncol + s) * V + c * 4) : (const void *)in,
+                           ok ? 16 : 0);
             }
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    issue(0);
+    issue(1);
+    issue(2);
+    int32_t Iacc[16];
+    for (int q = 0; q < nq; ++q) {
+        asm volatile("cp.async.wait_group 2;" ::: "memory");
         __syncwarp();
-        auto ld = [&](int r1, int j, int s) -> int32_t { return st[((r1 * 9 + j) * 8 + s) * 32 + lane]; };
+        const int r1 = q % 3;
+        int64_t A, B, v0;
+        task_coords(q / 3, A, B, v0);
+        const int32_t *st = reinterpret_cast<const int32_t *>(ring + (q % VF3_SLOTS) * VF3_GROUP_CHUNKS);
+        auto x = [&](int j, int s) -> int32_t { return st[(j * 8 + s) * 32 + lane]; };
         const int64_t v = v0 + lane;
-        if constexpr (!FINAL) {
-            int32_t *out = reinterpret_cast<int32_t *>(a.f.out) + ((A - a.ya0) * a.nB + B) * 64 * V + v;
-            vblock<3, int32_t>(ld, [&](int d, int32_t y) { out[(int64_t)d * V] = y; });
-        } else {
-            vblock<3, int32_t>(ld, [&](int d, int32_t y) { store_final(a.f, (uint64_t)(d * V + v), (int64_t)y); });
+        int32_t *out = nullptr;
+        if constexpr (!FINAL) out = reinterpret_cast<int32_t *>(a.f.out) + ((A - a.ya0) * a.nB + B) * 64 * V + v;
+        auto sink = [&](int d, int32_t y) {
+            if constexpr (!FINAL) out[(int64_t)d * V] = y;
+            else store_final(a.f, (uint64_t)(d * V + v), (int64_t)y);
+        };
+        if (r1 == 0) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) Iacc[k] = 0;
+        }
+        int32_t w[2][16];  // [b1][D2 D3]
+#pragma unroll
+        for (int b1 = 0; b1 < 2; ++b1) {
+            int32_t u[3][2][4];  // after qubit 3: [r2][b2][D3]
+#pragma unroll
+            for (int r2 = 0; r2 < 3; ++r2)
+#pragma unroll
+                for (int b2 = 0; b2 < 2; ++b2) {
+                    const int s0 = b1 * 4 + b2 * 2;
+                    q6to4<int32_t>(x(r2 * 3 + 0, s0), x(r2 * 3 + 0, s0 + 1), x(r2 * 3 + 1, s0), x(r2 * 3 + 1, s0 + 1),
+                                   x(r2 * 3 + 2, s0), x(r2 * 3 + 2, s0 + 1), u[r2][b2][0], u[r2][b2][1], u[r2][b2][2],
+                                   u[r2][b2][3]);
+                }
+#pragma unroll
+            for (int d3 = 0; d3 < 4; ++d3)
+                q6to4<int32_t>(u[0][0][d3], u[0][1][d3], u[1][0][d3], u[1][1][d3], u[2][0][d3], u[2][1][d3],
+                               w[b1][0 * 4 + d3], w[b1][1 * 4 + d3], w[b1][2 * 4 + d3], w[b1][3 * 4 + d3]);
         }
         __syncwarp();
+        issue(q + 3);  // this slot's data is in registers now
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            Iacc[k] += w[0][k] + w[1][k];
+            sink((r1 + 1) * 16 + k, w[0][k] - w[1][k]);
+        }
+        if (r1 == 2) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) sink(k, Iacc[k]);
+        }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ===========================================================================
@@ -992,7 +1048,7 @@ static cudaError_t launch_vfold(const VArgs &a, cudaStream_t s) {
 }
 
 static cudaError_t launch_vfold3(const VArgs &a, cudaStream_t s) {
-    const size_t smem = (size_t)VF3_WARPS * VF3_TASK_INTS * sizeof(int32_t);
+    const size_t smem = (size_t)VF3_WARPS * VF3_SLOTS * VF3_GROUP_CHUNKS * sizeof(int4);
     const int64_t tasks = a.nA * a.nB * (a.V >> 5);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + VF3_WARPS - 1) / VF3_WARPS,
                                                                 (int64_t)g_num_sms * 2));
