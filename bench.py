@@ -317,7 +317,7 @@ def run_b200(args):
     t_asm = e[2].elapsed_time(e[3]) / 1e3 / k
     pass1_bytes = c * 6.0**n  # algorithmic: every count read once (the Y1 write is not counted)
     q1 = min(n, 7)
-    tma = counts.dtype == torch.uint16 and shots <= 1213 and n >= 6 and os.environ.get("LRE_P1_TMA") == "1"
+    tma = counts.dtype == torch.uint16 and shots <= 1213 and n >= 6 and os.environ.get("LRE_P1") == "tma"
     p1_name = (f"tile_tma_kernel<{q1}> (pass 1, TMA ring)" if tma else f"tile_pass_kernel<{q1}> (pass 1, LDG)") \
         if n >= 6 else "vfold_kernel (pass 1)"
     achieved = pass1_bytes / t_pass1 / 1e9

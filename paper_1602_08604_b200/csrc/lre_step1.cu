@@ -26,6 +26,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include <vector>
 
@@ -160,6 +161,12 @@ __device__ __forceinline__ void load_wide(const int64_t *p, int32_t v[8]) {
         const longlong2 q = __ldcs(reinterpret_cast<const longlong2 *>(p) + i);
         v[2 * i] = (int32_t)q.x; v[2 * i + 1] = (int32_t)q.y;
     }
+}
+
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc), "r"(src_bytes)
+                 : "memory");
 }
 
 // packed word w = L + 65536 H (|L|,|H|,|L+-H| < 2^15): L - H and L + H
@@ -430,6 +437,232 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------------------
+// L2 split by the top core setting digit a1 (for the warp-parallel L2 of the
+// ring kernel): qubits c3 = (a3, b3) and c2 = (a2, b2, streamed over a2) in
+// registers, then the b1 half of qubit c1.  emit(r, v) receives the final
+// values with D1 = a1 + 1 (r = D1*16 + D2*4 + D3); icon(k, v) receives this
+// a1's contribution to the D1 = I value of k = D2*4 + D3.
+template <typename T, int STRIDE, typename Emit, typename Icon>
+__device__ __forceinline__ void l2_part(const T *st, int a1, Emit emit, Icon icon) {
+    int32_t Iacc[2][4];  // [b1][D3], D2 = I
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int d = 0; d < 4; ++d) Iacc[b][d] = 0;
+#pragma unroll
+    for (int a2 = 0; a2 < 3; ++a2) {
+        int32_t x[3][8];  // [a3][g = b1 b2 b3]
+#pragma unroll
+        for (int a3 = 0; a3 < 3; ++a3)
+#pragma unroll
+            for (int g = 0; g < 8; ++g) x[a3][g] = (int32_t)st[((a1 * 9 + a2 * 3 + a3) * 8 + g) * STRIDE];
+        int32_t u[2][2][4];  // [b1][b2][D3]
+#pragma unroll
+        for (int b1 = 0; b1 < 2; ++b1)
+#pragma unroll
+            for (int b2 = 0; b2 < 2; ++b2) {
+                const int g0 = b1 * 4 + b2 * 2;
+                q6to4<int32_t>(x[0][g0], x[0][g0 + 1], x[1][g0], x[1][g0 + 1], x[2][g0], x[2][g0 + 1], u[b1][b2][0],
+                               u[b1][b2][1], u[b1][b2][2], u[b1][b2][3]);
+            }
+#pragma unroll
+        for (int D3 = 0; D3 < 4; ++D3) {
+            Iacc[0][D3] += u[0][0][D3] + u[0][1][D3];
+            Iacc[1][D3] += u[1][0][D3] + u[1][1][D3];
+            const int32_t d0 = u[0][0][D3] - u[0][1][D3], d1 = u[1][0][D3] - u[1][1][D3];  // D2 = a2 + 1
+            emit((a1 + 1) * 16 + (a2 + 1) * 4 + D3, d0 - d1);
+            icon((a2 + 1) * 4 + D3, d0 + d1);
+        }
+    }
+#pragma unroll
+    for (int D3 = 0; D3 < 4; ++D3) {
+        emit((a1 + 1) * 16 + D3, Iacc[0][D3] - Iacc[1][D3]);
+        icon(D3, Iacc[0][D3] + Iacc[1][D3]);
+    }
+}
+
+// Store core value r (D1 D2 D3) of staged column col for sub-tile st: Q = 6
+// writes Y1 directly; Q = 7 combines the tile's top qubit (r1, b1): the
+// b1 = 0 half parks in tmp, X/Y/Z = tmp - v are final, I accumulates in oi
+// over r1.  Each (r, col) is owned by exactly one thread.
+template <int Q>
+__device__ __forceinline__ void p1_store(int32_t *out, const SubTile &st, int r, int col, int32_t v, int32_t *tmp,
+                                         int32_t *oi) {
+    if constexpr (Q == 6) {
+        out[r * 64] = v;
+    } else if (st.b1 == 0) {
+        tmp[r * 64 + col] = v;
+    } else {
+        const int32_t u = tmp[r * 64 + col];
+        const int32_t acc = (st.r1 == 0 ? 0 : oi[r * 64 + col]) + u + v;
+        if (st.r1 < 2) oi[r * 64 + col] = acc;
+        else out[r * 64] = acc;                    // top digit I
+        out[(st.r1 + 1) * 4096 + r * 64] = u - v;  // top digit X / Y / Z
+    }
+}
+
+template <int Q>
+__device__ __forceinline__ int32_t *p1_out(const P1Args &a, const SubTile &st, int col) {
+    return reinterpret_cast<int32_t *>(a.f.out) + (((st.aH - a.out_aH0) * a.C + st.c) << (2 * Q)) +
+           staged_col_to_dlo(col);
+}
+
+// Pass-1 tile kernel, cp.async-ring variant (uint16 counts, SMALL mode): one
+// CTA of 15 warps per SM, persistent.  Per sub-tile s (one __syncthreads):
+//   warps 0-6   L1(s): each thread streams the 9-row steps of its items
+//               through a private ring of three 144-byte shared-memory slots
+//               filled by cp.async, so steps q+1 and q+2 are in flight while
+//               step q computes (62 KB per SM continuously, no registers
+//               held), across sub-tile boundaries;
+//   warps 7-12  L2(s-1): staged column x top core digit a1 -> the D1 = a1+1
+//               values + I contributions (the single-thread-per-column L2 is
+//               a latency-bound chain of ~900 instructions);
+//   warps 13-14 I(s-2): the D1 = I values = sum of the three contributions.
+constexpr int RING_SLOT_BYTES = 9 * 16;
+constexpr int RING_THREAD_BYTES = 3 * RING_SLOT_BYTES;
+constexpr int RING_L1_WARPS = 7, RING_L2_WARPS = 6, RING_RED_WARPS = 2;
+constexpr int RING_THREADS = 32 * (RING_L1_WARPS + RING_L2_WARPS + RING_RED_WARPS);
+
+template <int Q> struct RingSmem {
+    static constexpr size_t STAGE = Stage<true>::BYTES;
+    static constexpr size_t EXTRA = P1Smem<Q, true>::EXTRA;
+    static constexpr size_t IRED = 2 * 3 * 16 * 64 * sizeof(int32_t);
+    static constexpr size_t RING = (size_t)P1_ITEMS * RING_THREAD_BYTES;
+    static constexpr size_t TOTAL = 2 * STAGE + EXTRA + IRED + RING;
+};
+
+template <int Q, int LOGN>
+__global__ void __launch_bounds__(RING_THREADS, 1) tile_ring_kernel(const P1Args a) {
+    using ST = Stage<true>;
+    using T = ST::T;
+    constexpr int STRIDE = ST::STRIDE;
+    constexpr int SUB = Q == 7 ? 6 : 1;
+    constexpr int64_t Q3 = Q == 7 ? 2187 : 729;
+    extern __shared__ __align__(16) unsigned char smem[];
+    int32_t *tmp = reinterpret_cast<int32_t *>(smem + 2 * ST::BYTES);
+    int32_t *oi = tmp + 64 * 64;
+    int32_t *ired = reinterpret_cast<int32_t *>(smem + 2 * ST::BYTES + RingSmem<Q>::EXTRA);  // [2][3][16][64]
+    unsigned char *ring = smem + 2 * ST::BYTES + RingSmem<Q>::EXTRA + RingSmem<Q>::IRED;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int64_t ntiles = a.naH * a.C;
+    const int my_tiles = (int64_t)blockIdx.x < ntiles ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+    const int S = my_tiles * SUB;
+    const uint16_t *counts = reinterpret_cast<const uint16_t *>(a.counts);
+    const int rowlen = LOGN > 0 ? (1 << LOGN) : (int)a.rowlen;
+    const bool l1 = tid < P1_ITEMS;
+    const int rb = tid >> 3, g = tid & 7;
+    unsigned char *myring = ring + (l1 ? tid : 0) * RING_THREAD_BYTES;
+
+    auto item_base = [&](int s) -> const uint16_t * {
+        const SubTile st = subtile_of<Q>(a, s);
+        const int64_t row = st.aH * Q3 + (Q == 7 ? st.r1 * 729 : 0) + rb * 27 - a.row_base;
+        const int64_t col = (st.c << Q) + (Q == 7 ? st.b1 * 64 : 0) + g * 8;
+        return counts + row * (int64_t)rowlen + col;
+    };
+    // step q = 3 s + a3: the 9 rows (a1, a2) of step a3 of sub-tile s
+    const int nq = 3 * S;
+    const uint16_t *ib_issue = nullptr;
+    int s_issue = -1;
+    auto issue = [&](int q) {
+        if (q < nq) {
+            const int s = q / 3, a3 = q % 3;
+            if (s != s_issue) {
+                ib_issue = item_base(s);
+                s_issue = s;
+            }
+            unsigned char *slot = myring + (q % 3) * RING_SLOT_BYTES;
+#pragma unroll
+            for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+                for (int a2 = 0; a2 < 3; ++a2)
+                    cp_async16(slot + (a1 * 3 + a2) * 16, ib_issue + (a1 * 9 + a2 * 3 + a3) * rowlen, 16);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+
+    if (l1) {
+        issue(0);
+        issue(1);
+    }
+    for (int s = 0; s < S + 2; ++s) {
+        if (warp < RING_L1_WARPS) {
+            if (s < S && l1) {
+                T *rec = reinterpret_cast<T *>(smem + (s & 1) * ST::BYTES) + tid * STRIDE;
+                uint32_t Iacc[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) Iacc[k] = 0;
+#pragma unroll
+                for (int a3 = 0; a3 < 3; ++a3) {
+                    const int q = 3 * s + a3;
+                    issue(q + 2);
+                    asm volatile("cp.async.wait_group 2;" ::: "memory");
+                    const unsigned char *slot = myring + (q % 3) * RING_SLOT_BYTES;
+                    uint32_t x[3][3][4];
+#pragma unroll
+                    for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+                        for (int a2 = 0; a2 < 3; ++a2) {
+                            const uint4 u = *reinterpret_cast<const uint4 *>(slot + (a1 * 3 + a2) * 16);
+                            x[a1][a2][0] = u.x; x[a1][a2][1] = u.y; x[a1][a2][2] = u.z; x[a1][a2][3] = u.w;
+                        }
+                    uint32_t y[4][3][2];  // [D4][a2][b5]
+#pragma unroll
+                    for (int a2 = 0; a2 < 3; ++a2)
+#pragma unroll
+                        for (int b5 = 0; b5 < 2; ++b5)
+                            q6to4<uint32_t>(x[0][a2][b5], x[0][a2][2 + b5], x[1][a2][b5], x[1][a2][2 + b5],
+                                            x[2][a2][b5], x[2][a2][2 + b5], y[0][a2][b5], y[1][a2][b5], y[2][a2][b5],
+                                            y[3][a2][b5]);
+                    int32_t v[16];
+#pragma unroll
+                    for (int D4 = 0; D4 < 4; ++D4) {
+                        uint32_t z[4];
+                        q6to4<uint32_t>(y[D4][0][0], y[D4][0][1], y[D4][1][0], y[D4][1][1], y[D4][2][0],
+                                        y[D4][2][1], z[0], z[1], z[2], z[3]);
+#pragma unroll
+                        for (int D5 = 0; D5 < 4; ++D5) {
+                            Iacc[D4 * 4 + D5] += z[D5];
+                            v[D4 * 4 + D5] = packed_diff(z[D5]);
+                        }
+                    }
+                    stage_record<true>(rec, a3 + 1, v);
+                }
+                int32_t v[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v[k] = packed_sum(Iacc[k]);
+                stage_record<true>(rec, 0, v);
+            }
+        } else if (warp < RING_L1_WARPS + RING_L2_WARPS) {
+            if (s >= 1 && s <= S) {
+                const int u = tid - 32 * RING_L1_WARPS;
+                const int a1 = u >> 6, col = u & 63;
+                const SubTile st = subtile_of<Q>(a, s - 1);
+                const T *stage = reinterpret_cast<const T *>(smem + ((s - 1) & 1) * ST::BYTES) + col;
+                int32_t *out = p1_out<Q>(a, st, col);
+                int32_t *ic = ired + (((s - 1) & 1) * 3 + a1) * 16 * 64 + col;
+                l2_part<T, STRIDE>(
+                    stage, a1, [&](int r, int32_t v) { p1_store<Q>(out, st, r, col, v, tmp, oi); },
+                    [&](int k, int32_t v) { ic[k * 64] = v; });
+            }
+        } else {
+            if (s >= 2) {
+                const int col = tid - 32 * (RING_L1_WARPS + RING_L2_WARPS);
+                const SubTile st = subtile_of<Q>(a, s - 2);
+                int32_t *out = p1_out<Q>(a, st, col);
+                const int32_t *ic = ired + ((s - 2) & 1) * 3 * 16 * 64 + col;
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    p1_store<Q>(out, st, k, col, ic[k * 64] + ic[(16 + k) * 64] + ic[(32 + k) * 64], tmp, oi);
+            }
+        }
+        __syncthreads();
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // ===========================================================================
@@ -721,12 +954,6 @@ constexpr int VF3_WARPS = 4;
 constexpr int VF3_GROUP_CHUNKS = 72 * 8;  // 16-byte chunks per r1 group (72 lines x 128 B)
 constexpr int VF3_SLOTS = 3;
 
-__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, int src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
-                 "l"(gsrc), "r"(src_bytes)
-                 : "memory");
-}
-
 template <bool FINAL>
 __global__ void __launch_bounds__(32 * VF3_WARPS, 2) vfold3_kernel(const VArgs a) {
     extern __shared__ __align__(16) int4 vsm4[];
@@ -923,11 +1150,13 @@ static int g_num_sms = 0;
 static bool g_pow3_ready = false;
 
 static bool g_disable_tma;
+static int g_p1_variant = 1;  // 1 = LDG (default), 0 = cp.async ring (LRE_P1=ring), 2 = TMA (LRE_P1=tma)
 
 static cudaError_t ensure_init() {
     if (!g_pow3_ready) {
-        const char *env = getenv("LRE_P1_TMA");
-        g_disable_tma = !(env && env[0] == '1');
+        const char *env = getenv("LRE_P1");
+        g_p1_variant = env && !strcmp(env, "ring") ? 0 : env && !strcmp(env, "tma") ? 2 : 1;
+        g_disable_tma = g_p1_variant != 2;
         g_pow3_ready = true;
     }
     if (!g_num_sms) {
@@ -952,19 +1181,39 @@ static cudaError_t launch_tile(const P1Args &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <int Q, int LOGN>
+static cudaError_t launch_ring(const P1Args &a, cudaStream_t s) {
+    auto kern = tile_ring_kernel<Q, LOGN>;
+    const size_t smem = RingSmem<Q>::TOTAL;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t ntiles = a.naH * a.C;
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms);
+    kern<<<(unsigned)grid, RING_THREADS, smem, s>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+
+template <int Q, int LOGN>
+static cudaError_t launch_u16_small(const P1Args &a, cudaStream_t s) {
+    if (g_p1_variant == 1) return launch_tile<Q, true, uint16_t, LOGN>(a, s);
+    return launch_ring<Q, LOGN>(a, s);
+}
+
 // uint16 SMALL tiles (the benchmark format) get a compile-time row length
 template <int Q>
 static cudaError_t tile_u16_small(const P1Args &a, cudaStream_t s) {
     switch (a.rowlen) {
-    case 1 << 7: return launch_tile<Q, true, uint16_t, 7>(a, s);
-    case 1 << 8: return launch_tile<Q, true, uint16_t, 8>(a, s);
-    case 1 << 9: return launch_tile<Q, true, uint16_t, 9>(a, s);
-    case 1 << 10: return launch_tile<Q, true, uint16_t, 10>(a, s);
-    case 1 << 11: return launch_tile<Q, true, uint16_t, 11>(a, s);
-    case 1 << 12: return launch_tile<Q, true, uint16_t, 12>(a, s);
-    case 1 << 13: return launch_tile<Q, true, uint16_t, 13>(a, s);
-    case 1 << 14: return launch_tile<Q, true, uint16_t, 14>(a, s);
-    default: return launch_tile<Q, true, uint16_t>(a, s);
+    case 1 << 7: return launch_u16_small<Q, 7>(a, s);
+    case 1 << 8: return launch_u16_small<Q, 8>(a, s);
+    case 1 << 9: return launch_u16_small<Q, 9>(a, s);
+    case 1 << 10: return launch_u16_small<Q, 10>(a, s);
+    case 1 << 11: return launch_u16_small<Q, 11>(a, s);
+    case 1 << 12: return launch_u16_small<Q, 12>(a, s);
+    case 1 << 13: return launch_u16_small<Q, 13>(a, s);
+    case 1 << 14: return launch_u16_small<Q, 14>(a, s);
+    default: return launch_u16_small<Q, 0>(a, s);
     }
 }
 
@@ -1020,7 +1269,7 @@ static cudaError_t launch_tma(const P1Args &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-// pass 1 uses the LDG variant; LRE_P1_TMA=1 selects the TMA-ring variant (measured slower)
+// pass-1 variant for uint16 SMALL tiles: LRE_P1=ldg (default) | ring | tma (A/B measurements)
 
 static cudaError_t run_tile(int q, int small, int dtype, const P1Args &a, cudaStream_t s) {
     if (small && dtype == LRE_U16 && !g_disable_tma && (a.rowlen * 2) % 16 == 0 &&

@@ -27,7 +27,7 @@ e1.record(s); e1.synchronize()
 print(f"passes 2.. {e0.elapsed_time(e1)/K:.3f} ms")
 ''' % ROOT
 n = sys.argv[1]; shots = sys.argv[2] if len(sys.argv) > 2 else "1000"
-for env in ({}, {"LRE_P1_TMA": "1"}):
+for env in ({}, {"LRE_P1": "ring"}):
     try:
         r = subprocess.run([sys.executable, "-c", CODE, n, shots], env={**os.environ, **env}, capture_output=True,
                            text=True, timeout=240)

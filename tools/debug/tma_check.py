@@ -24,7 +24,7 @@ ref = C.numerators(counts, n)
 print("n", n, "exact", bool((got == ref).all()), "mismatches", int((got != ref).sum()))
 ''' % ROOT
 for n in (int(x) for x in sys.argv[1:]):
-    for env in ({}, {"LRE_P1_TMA": "1"}):
+    for env in ({}, {"LRE_P1": "ring"}, {"LRE_P1": "tma"}):
         try:
             r = subprocess.run([sys.executable, "-c", CODE, str(n)], env={**os.environ, **env}, capture_output=True,
                                text=True, timeout=90)
