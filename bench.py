@@ -318,8 +318,10 @@ def run_b200(args):
     pass1_bytes = c * 6.0**n  # algorithmic: every count read once (the Y1 write is not counted)
     q1 = min(n, 7)
     tma = counts.dtype == torch.uint16 and shots <= 1213 and n >= 6 and os.environ.get("LRE_P1") == "tma"
-    p1_name = (f"tile_tma_kernel<{q1}> (pass 1, TMA ring)" if tma else f"tile_pass_kernel<{q1}> (pass 1, LDG)") \
-        if n >= 6 else "vfold_kernel (pass 1)"
+    variant = os.environ.get("LRE_P1", "ldg")
+    p1_name = (f"tile_tma_kernel<{q1}> (pass 1, TMA ring)" if tma else
+               f"tile_ring_kernel<{q1}> (pass 1, cp.async ring)" if variant == "ring" and counts.dtype == torch.uint16
+               else f"tile_pass_kernel<{q1}> (pass 1, LDG)") if n >= 6 else "vfold_kernel (pass 1)"
     achieved = pass1_bytes / t_pass1 / 1e9
     traffic = traffic_from_profiles(n)
     whole = algorithmic_bytes(n, c) / t_step / 1e9
