@@ -37,11 +37,14 @@
 
 namespace lre {
 
-// theta = N * c_fac[zc], c_fac[zc] = 2^{-n/2} / shots / 3^zc (set per launch
+// theta = N * g_fac[zc], g_fac[zc] = 2^{-n/2} / shots / 3^zc (set per launch
 // sequence): one multiply per output instead of two fp64 divisions; relative
 // error <= 2 ulp, far inside the 1e-10 parity bar (the integer numerators
 // N stay exact).
-__constant__ double c_fac[33];
+// (global memory, read with __ldg: lanes of a warp use different zc, and
+// divergent __constant__ reads serialise — that alone made the final pass 2.4x
+// slower than its bytes)
+__device__ double g_fac[33];
 
 // ===========================================================================
 // epilogue shared by both kernels
@@ -59,14 +62,18 @@ struct Final {
 
 // store a finished numerator at natural Pauli index `nat`
 __device__ __forceinline__ void store_final(const Final &f, uint64_t nat, int64_t v) {
-    uint32_t m, a;
-    natural_to_ma(nat, m, a);
-    const uint64_t pos = f.layout == LRE_LAYOUT_MASK_MAJOR ? (((uint64_t)m << f.n) | a) : nat;
+    uint64_t pos = nat;
+    if (f.layout == LRE_LAYOUT_MASK_MAJOR) {
+        uint32_t m, a;
+        natural_to_ma(nat, m, a);
+        pos = ((uint64_t)m << f.n) | a;
+    }
     if (f.kind == OUT_NUM) {
         reinterpret_cast<int64_t *>(f.out)[pos] = v;
     } else {
-        const int zc = f.n - __popc(m | a);
-        reinterpret_cast<double *>(f.out)[pos] = (double)v * c_fac[zc];
+        // zc = number of I (zero) base-4 digits of the natural index
+        const int zc = f.n - __popcll((nat | (nat >> 1)) & 0x5555555555555555ull);
+        reinterpret_cast<double *>(f.out)[pos] = (double)v * __ldg(&g_fac[zc]);
     }
 }
 
@@ -1356,7 +1363,7 @@ static cudaError_t run_vfold(int q, int in_dtype, int acc64, const VArgs &a, cud
 static int g_fac_n = -1, g_fac_dev = -1;
 static int64_t g_fac_shots = -1;
 
-// c_fac for (n, shots); uploaded only when they change (stream-ordered)
+// g_fac for (n, shots); uploaded only when they change (stream-ordered)
 static cudaError_t set_factors(int n, int64_t shots, cudaStream_t s) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -1368,7 +1375,7 @@ static cudaError_t set_factors(int n, int64_t shots, cudaStream_t s) {
         fac[zc] = (double)((long double)scale / (long double)shots / (long double)p3);
         p3 *= 3.0;
     }
-    cudaError_t e = cudaMemcpyToSymbolAsync(c_fac, fac, sizeof(fac), 0, cudaMemcpyHostToDevice, s);
+    cudaError_t e = cudaMemcpyToSymbolAsync(g_fac, fac, sizeof(fac), 0, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return e;
     e = cudaStreamSynchronize(s);  // fac[] is static host memory reused by the next call
     if (e != cudaSuccess) return e;
