@@ -98,63 +98,3 @@ class ShardedLRE:
         num = self.c.partial_numerators(counts, count_dtype)
         dist.reduce_scatter_tensor(self.c.recv, num, op=dist.ReduceOp.SUM, group=self.group)
         return self.c.finalize_and_assemble()
-
-
-def bench_main(args, rank: int, world: int, local: int):
-    """bench.py --gpus N under torchrun: max-over-ranks device time per reconstruction."""
-    import json
-    import statistics
-
-    import torch
-    import torch.distributed as dist
-
-    import paper_1602_08604_b200 as lre
-    from paper_1602_08604_b200 import _lib
-    from paper_1602_08604_b200.simulate import generate_device_counts
-
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    n, shots, seed = args.n, args.shots, args.seed
-    q = int(_lib.load().lre_shard_quantum(n))
-    lo, hi = shard_ranges(n, world, q)[rank]
-    st = lre.StateDescriptor(args.state, n)
-    counts = generate_device_counts(st, shots, seed=seed, w_begin=lo, w_end=hi, device=dev)
-    rec = lre.DeviceRecord(n=n, shots=shots, counts=counts, w_begin=lo, seed=seed, state=st.label()).validate()
-    comp = DeviceCompute(n, shots, lo, hi, world, rank, dev)
-    runner = ShardedLRE(comp)
-    for _ in range(max(args.warmup, 3)):
-        runner.step(counts, rec.lre_dtype)
-    torch.cuda.synchronize()
-    s = torch.cuda.current_stream(dev)
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    l0 = _lib.launch_count()
-    dist.barrier()
-    torch.cuda.synchronize()
-    evs[0].record(s)
-    for i in range(args.steps):
-        runner.step(counts, rec.lre_dtype)
-        evs[i + 1].record(s)
-    torch.cuda.synchronize()
-    dist.barrier()
-    per = torch.tensor([evs[i].elapsed_time(evs[i + 1]) / 1e3 for i in range(args.steps)], device=dev)
-    dist.all_reduce(per, op=dist.ReduceOp.MAX)
-    t = statistics.median(per.cpu().tolist())
-    launches = _lib.launch_count() - l0
-    if rank == 0:
-        c = counts.element_size()
-        b = c * 6.0**n + 32.0 * 4.0**n
-        print(json.dumps({
-            "metric": "14-qubit LRE reconstruction seconds at 1/2/4/8 B200; achieved HBM GB/s",
-            "value": t, "unit": "s", "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3),
-            "ms_per_step": t * 1e3, "higher_is_better": False, "scaling": "strong",
-            "vs_baseline": t / ((2.78 + 0.08) * 3600.0) if n == 14 else None,
-            "dtype": "i32/i64 exact integer folds, f64 theta/mu",
-            "data": "synthetic: device generator per shard, Philox4x32-10 per (seed, setting)",
-            "config": {"workload": f"C5: n={n} {args.state.upper()}, settings sharded over {world} GPUs, "
-                                   f"int64 numerator reduce-scatter by X-mask", "n": n, "shots": shots,
-                       "parallelism": f"settings/{world}, masks/{world}"},
-            "whole_path": {"algorithmic_bytes": b, "achieved_GBps": b / t / 1e9},
-            "gpu_launches": int(launches),
-        }))
-    dist.destroy_process_group()
