@@ -420,29 +420,93 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
     const int S = my_tiles * SUB;
     const Tin *counts = reinterpret_cast<const Tin *>(a.counts);
     const int rowlen = LOGN > 0 ? (1 << LOGN) : (int)a.rowlen;
+    const bool l1 = warp < P1_L1_WARPS && tid < P1_ITEMS;
+    const int rb = tid >> 3, g = tid & 7;
 
-    for (int s = 0; s <= S; ++s) {
-        if (warp < P1_L1_WARPS) {
-            if (s < S && tid < P1_ITEMS) {
-                const SubTile st = subtile_of<Q>(a, s);
-                const int rb = tid >> 3, g = tid & 7;
-                const int64_t row = st.aH * Q3 + (Q == 7 ? st.r1 * 729 : 0) + rb * 27 - a.row_base;
-                const int64_t col = (st.c << Q) + (Q == 7 ? st.b1 * 64 : 0) + g * 8;
-                const Tin *base = counts + row * (int64_t)rowlen + col;
+    auto item_base = [&](int s) -> const Tin * {
+        const SubTile st = subtile_of<Q>(a, s);
+        const int64_t row = st.aH * Q3 + (Q == 7 ? st.r1 * 729 : 0) + rb * 27 - a.row_base;
+        const int64_t col = (st.c << Q) + (Q == 7 ? st.b1 * 64 : 0) + g * 8;
+        return counts + row * (int64_t)rowlen + col;
+    };
+    auto load_step = [&](const Tin *base, int a3, uint32_t(&x)[3][3][4]) {
+#pragma unroll
+        for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+            for (int a2 = 0; a2 < 3; ++a2) load_packed(base + (a1 * 9 + a2 * 3 + a3) * rowlen, x[a1][a2]);
+    };
+
+    // L1 and L2 warps run separate loops with the same barrier sequence, so
+    // the L1 loop's registers that live across sub-tiles (the prefetched
+    // next step) are not allocated in the L2 code.
+    if (warp < P1_L1_WARPS) {
+        // SMALL: the loads of the next 9-row step are issued as soon as the
+        // first qubit stage has consumed the current step's words (reusing
+        // their registers), so they fly during the rest of this step's
+        // compute — the next sub-tile's first step included.
+        uint32_t x[3][3][4];
+        const Tin *base = nullptr;
+        if constexpr (SMALL) {
+            if (l1 && S > 0) {
+                base = item_base(0);
+                load_step(base, 0, x);
+            }
+        }
+        for (int s = 0; s <= S; ++s) {
+            if (s < S && l1) {
                 T *rec = reinterpret_cast<T *>(smem + (s & 1) * ST::BYTES) + tid * STRIDE;
-                auto sink = [&](int D6, const int32_t(&v)[16]) { stage_record<SMALL>(rec, D6, v); };
                 if constexpr (SMALL) {
-                    l1_small([&](int j, uint32_t(&w)[4]) { load_packed(base + j * rowlen, w); }, sink);
+                    const Tin *next_base = s + 1 < S ? item_base(s + 1) : nullptr;
+                    uint32_t Iacc[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) Iacc[k] = 0;
+#pragma unroll
+                    for (int a3 = 0; a3 < 3; ++a3) {
+                        uint32_t y[4][3][2];  // [D4][a2][b5]: qubit (a1, b4)
+#pragma unroll
+                        for (int a2 = 0; a2 < 3; ++a2)
+#pragma unroll
+                            for (int b5 = 0; b5 < 2; ++b5)
+                                q6to4<uint32_t>(x[0][a2][b5], x[0][a2][2 + b5], x[1][a2][b5], x[1][a2][2 + b5],
+                                                x[2][a2][b5], x[2][a2][2 + b5], y[0][a2][b5], y[1][a2][b5],
+                                                y[2][a2][b5], y[3][a2][b5]);
+                        if (a3 < 2) load_step(base, a3 + 1, x);
+                        else if (next_base) load_step(next_base, 0, x);
+                        int32_t v[16];
+#pragma unroll
+                        for (int D4 = 0; D4 < 4; ++D4) {
+                            uint32_t z[4];
+                            q6to4<uint32_t>(y[D4][0][0], y[D4][0][1], y[D4][1][0], y[D4][1][1], y[D4][2][0],
+                                            y[D4][2][1], z[0], z[1], z[2], z[3]);
+#pragma unroll
+                            for (int D5 = 0; D5 < 4; ++D5) {
+                                Iacc[D4 * 4 + D5] += z[D5];
+                                v[D4 * 4 + D5] = packed_diff(z[D5]);
+                            }
+                        }
+                        stage_record<true>(rec, a3 + 1, v);
+                    }
+                    int32_t v[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) v[k] = packed_sum(Iacc[k]);
+                    stage_record<true>(rec, 0, v);
+                    base = next_base;
                 } else {
-                    l1_wide([&](int j, int32_t(&w)[8]) { load_wide(base + j * rowlen, w); }, sink);
+                    const Tin *ib = item_base(s);
+                    l1_wide([&](int j, int32_t(&w)[8]) { load_wide(ib + j * rowlen, w); },
+                            [&](int D6, const int32_t(&v)[16]) { stage_record<SMALL>(rec, D6, v); });
                 }
             }
-        } else if (s > 0) {
-            l2_subtile<Q, SMALL>(a, subtile_of<Q>(a, s - 1),
-                                 reinterpret_cast<const T *>(smem + ((s - 1) & 1) * ST::BYTES),
-                                 tid - 32 * P1_L1_WARPS, tmp, oi);
+            asm volatile("bar.sync 0;" ::: "memory");
         }
-        __syncthreads();
+    } else {
+        for (int s = 0; s <= S; ++s) {
+            if (s > 0)
+                l2_subtile<Q, SMALL>(a, subtile_of<Q>(a, s - 1),
+                                     reinterpret_cast<const T *>(smem + ((s - 1) & 1) * ST::BYTES),
+                                     tid - 32 * P1_L1_WARPS, tmp, oi);
+            asm volatile("bar.sync 0;" ::: "memory");
+        }
     }
 }
 
