@@ -352,6 +352,29 @@ def run_b200(args):
         else:
             e2e = {"value": None, "unit": "s", "skipped": f"host RAM {avail >> 30} GiB < record {host_bytes >> 30} GiB"}
 
+    # --- step (iii), adjacent to the hot path and timed separately (north star):
+    # Hermitian eigensolve (cuSOLVER through torch.linalg.eigh) + simplex projection
+    step3 = None
+    if not args.no_step3:
+        rec = counts = None  # free the record (157 GB at n = 14) for the eigensolver's workspace
+        torch.cuda.empty_cache()
+        try:
+            warm = torch.eye(64, dtype=torch.complex128, device=dev) / 64  # cuSOLVER handle + module load
+            lre.step_three_project(warm)
+            torch.cuda.synchronize()
+            e3 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            e3[0].record(s)
+            rho, evals = lre.step_three_project(plan.mu)
+            e3[1].record(s)
+            torch.cuda.synchronize()
+            step3 = {"value": e3[0].elapsed_time(e3[1]) / 1e3, "unit": "s", "what": "step_three_project(mu): "
+                     "Hermiticity/trace checks + torch.linalg.eigh (cuSOLVER, library code) + simplex projection + "
+                     "V diag(lambda) V^H; not part of value", "projected": rho is not plan.mu,
+                     }
+            del rho, evals
+        except Exception as exc:
+            step3 = {"value": None, "unit": "s", "error": f"{type(exc).__name__}: {str(exc)[:160]}"}
+
     line = {
         "metric": METRIC,
         "value": t_step,
@@ -377,6 +400,7 @@ def run_b200(args):
                        "t_pass1_s": t_pass1, "t_pass2_s": t_rest1, "t_assemble_s": t_asm},
         "cpu_baseline": base,
         "e2e": e2e,
+        "step3": step3,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -574,6 +598,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-step3", action="store_true", help="skip the separately timed step (iii) eigen-projection")
     ap.add_argument("--force-dist", action="store_true", help="run the torch.distributed path even at world size 1")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -120,6 +120,7 @@ struct P1Args {
     int64_t out_aH0;     // first tile row group held by the output buffer
     int64_t C;           // column tiles, 2^(n-Q)
     Final f;             // f.kind == OUT_INTER: Y1 int32 tile-major
+    int debug_no_l2;     // diagnostics only (LRE_P1_DEBUG=noL2): skip the L2 work, output invalid
 };
 
 // --- packed loads: 8 consecutive counts -> 4 words (c[2k] | c[2k+1] << 16) ---
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
         }
     } else {
         for (int s = 0; s <= S; ++s) {
-            if (s > 0)
+            if (s > 0 && !a.debug_no_l2)
                 l2_subtile<Q, SMALL>(a, subtile_of<Q>(a, s - 1),
                                      reinterpret_cast<const T *>(smem + ((s - 1) & 1) * ST::BYTES),
                                      tid - 32 * P1_L1_WARPS, tmp, oi);
@@ -1481,6 +1482,10 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             a.C = ipow(2, R - ps.q);
             a.f = f;
             a.f.kind = OUT_INTER;
+            {
+                const char *dbg = getenv("LRE_P1_DEBUG");
+                a.debug_no_l2 = dbg && !strcmp(dbg, "noL2");
+            }
             if (fin) a.f.out = ws;  // single-pass plan: int32 tile (natural order), converted below
             e = run_tile(ps.q, ps.small, ps.in_dtype, a, stream);
             if (e == cudaSuccess && fin) {
