@@ -120,7 +120,8 @@ struct P1Args {
     int64_t out_aH0;     // first tile row group held by the output buffer
     int64_t C;           // column tiles, 2^(n-Q)
     Final f;             // f.kind == OUT_INTER: Y1 int32 tile-major
-    int debug_no_l2;     // diagnostics only (LRE_P1_DEBUG=noL2): skip the L2 work, output invalid
+    int debug_no_l2;     // diagnostics only (LRE_P1_DEBUG=noL2 / noL1): skip L2 / L1 work, output invalid
+    int debug_no_l1;
 };
 
 // --- packed loads: 8 consecutive counts -> 4 words (c[2k] | c[2k+1] << 16) ---
@@ -454,7 +455,7 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
             }
         }
         for (int s = 0; s <= S; ++s) {
-            if (s < S && l1) {
+            if (s < S && l1 && !a.debug_no_l1) {
                 T *rec = reinterpret_cast<T *>(smem + (s & 1) * ST::BYTES) + tid * STRIDE;
                 if constexpr (SMALL) {
                     const Tin *next_base = s + 1 < S ? item_base(s + 1) : nullptr;
@@ -1485,6 +1486,7 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             {
                 const char *dbg = getenv("LRE_P1_DEBUG");
                 a.debug_no_l2 = dbg && !strcmp(dbg, "noL2");
+                a.debug_no_l1 = dbg && !strcmp(dbg, "noL1");
             }
             if (fin) a.f.out = ws;  // single-pass plan: int32 tile (natural order), converted below
             e = run_tile(ps.q, ps.small, ps.in_dtype, a, stream);
