@@ -120,12 +120,16 @@ def baseline_settings(n: int) -> int:
 
 
 def cpu_baseline(n: int, shots: int, seed: int, counts_rows=None, budget_s: float = 20.0):
-    """Extrapolated seconds of the reference LRE (steps i+ii) on the host cores.
+    """Seconds of the reference LRE (steps i+ii) on the host cores, from a bounded sample.
 
-    Step (i): the C port (oracle/lre_oracle.c, private per-thread 4^n
-    partials, pipeline.py:62-138) on S and 2S settings -> fixed + per-setting
-    cost, extrapolated to 3^n settings.  Step (ii): per-mask cost on M masks
-    extrapolated to 2^n masks (pipeline.py:141-161).
+    Step (i): the C port of the reference (oracle/lre_oracle.c: per-setting
+    WHT + scatter into private per-worker 4^n partials, ordered merge,
+    pipeline.py:62-138) on 2S sampled settings, as a cost model: one-time
+    fixed cost (zero-filling the workers' partials + merge) + steady-state
+    seconds per setting per worker x 3^n / workers
+    (lre_oracle_step1_cost; validated against full runs, see
+    profiles/README.md).  Step (ii): per-mask cost on M masks extrapolated to
+    2^n masks (pipeline.py:141-161).
     """
     from oracle import c_oracle as C
     from oracle import lre_oracle as O
@@ -135,14 +139,8 @@ def cpu_baseline(n: int, shots: int, seed: int, counts_rows=None, budget_s: floa
     S = baseline_settings(n)
     rows = counts_rows if counts_rows is not None and counts_rows.shape[0] >= 2 * S else \
         O.sample_ghz_counts(n, shots, seed, 0, 2 * S)
-    t = []
-    for k in (S, 2 * S):
-        t0 = time.perf_counter()
-        C.step1_raw(rows[:k], n, shots, 0, threads)
-        t.append(time.perf_counter() - t0)
-    slope = max((t[1] - t[0]) / S, t[1] / (2 * S) * 0.5)
-    fixed = max(t[0] - slope * S, 0.0)
-    t_step1 = fixed + slope * 3**n
+    fixed, per = C.step1_cost(rows[: 2 * S], n, shots, 0, threads)
+    t_step1 = fixed + per * 3**n / threads
     theta = np.random.default_rng(0).standard_normal(4**n) * 2.0 ** (-n)
     M = max(threads, min(d, int(4e6 // d) * threads // 4 or threads))
     t0 = time.perf_counter()
@@ -154,9 +152,10 @@ def cpu_baseline(n: int, shots: int, seed: int, counts_rows=None, budget_s: floa
         "unit": "s",
         "cores": threads,
         "kind": "port",
-        "sample": (f"n={n} GHZ, step (i) on {S} and {2 * S} of {3**n} settings (fixed {fixed:.2f} s + "
-                   f"{slope * 1e6:.1f} us/setting), step (ii) on {M} of {d} masks; C port of "
-                   f"_kernels.accumulate_fast + step_two_assemble, {threads} threads"),
+        "sample": (f"n={n} GHZ, step (i) on {2 * S} of {3**n} settings: fixed {fixed:.2f} s (zeroing {threads} private "
+                   f"4^n partials + ordered merge) + {per * 1e6:.1f} us per setting per worker (steady state); "
+                   f"step (ii) on {M} of {d} masks; C port of _kernels.accumulate_fast + step_two_assemble, "
+                   f"{threads} threads"),
         "t_step1_s": t_step1,
         "t_step2_s": t_step2,
     }

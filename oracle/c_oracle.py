@@ -35,6 +35,7 @@ def lib():
         L.lre_oracle_gram_divide.argtypes = [vp, c_int]
         L.lre_oracle_step2_masks.argtypes = [vp, c_int, i64, i64, c_int, vp]
         L.lre_oracle_max_threads.restype = c_int
+        L.lre_oracle_step1_cost.argtypes = [vp, c_int, c_int, i64, i64, i64, c_int, vp, vp]
         _lib = L
     return _lib
 
@@ -91,3 +92,18 @@ def step_two(theta: np.ndarray, n: int, threads=None) -> np.ndarray:
     for m in range(d):
         mu[rows, rows ^ m] = diag[m]
     return mu
+
+
+def step1_cost(counts: np.ndarray, n: int, shots: int, w_begin: int = 0, threads=None):
+    """(fixed_s, per_setting_per_worker_s) of the reference step (i) on `threads`
+    workers, measured on this sample with the partials pre-faulted (see
+    lre_oracle.c:lre_oracle_step1_cost)."""
+    counts = np.ascontiguousarray(counts)
+    fixed = ctypes.c_double(0.0)
+    per = ctypes.c_double(0.0)
+    rc = lib().lre_oracle_step1_cost(counts.ctypes.data, _DTYPES[counts.dtype], n, int(shots), int(w_begin),
+                                     int(w_begin) + counts.shape[0], _threads(threads), ctypes.byref(fixed),
+                                     ctypes.byref(per))
+    if rc:
+        raise MemoryError("oracle step1 allocation failed")
+    return fixed.value, per.value

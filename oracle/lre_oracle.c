@@ -141,6 +141,87 @@ int lre_oracle_step1_raw(const void *counts, int dtype, int n, int64_t shots,
     return 0;
 }
 
+/*
+ * Cost model of lre_oracle_step1_raw on `threads` workers for the CPU
+ * baseline (bench.py), measured on a sample of settings [w_begin, w_end):
+ *   fixed_s      one-time costs of a full run: zero-filling the `threads`
+ *                private 4**n partials (calloc pages are faulted in on first
+ *                touch; the reference's np.zeros behaves the same) and the
+ *                ordered merge (pipeline.py:135-137);
+ *   per_row_s    steady-state seconds per setting per worker, measured on the
+ *                sample with the partials already touched (in a full run the
+ *                page faults are paid once, not per sampled setting).
+ * A full run is then fixed_s + per_row_s * settings / threads.
+ */
+int lre_oracle_step1_cost(const void *counts, int dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end,
+                          int threads, double *fixed_s, double *per_row_s) {
+    const int64_t d = (int64_t)1 << n;
+    const int64_t size = (int64_t)1 << (2 * n);
+    const double scale = pow(2.0, -n / 2.0);
+    const double fshots = (double)shots;
+    const int64_t total = w_end - w_begin;
+    if (threads < 1) threads = 1;
+    if (threads > total) threads = (int)(total > 0 ? total : 1);
+    double **partials = (double **)calloc((size_t)threads, sizeof(double *));
+    if (!partials) return 1;
+    int failed = 0;
+    double t_touch = 0.0, t_rows = 0.0;
+#pragma omp parallel num_threads(threads)
+    {
+        int tid = omp_get_thread_num();
+        int64_t a = (int64_t)((double)total * tid / threads);
+        int64_t b = (int64_t)((double)total * (tid + 1) / threads);
+        double t0 = omp_get_wtime();
+        double *raw = (double *)calloc((size_t)size, sizeof(double));
+        if (raw) memset(raw, 0, (size_t)size * sizeof(double));  /* fault every page in */
+#pragma omp barrier
+        double t1 = omp_get_wtime();
+        double *buf = (double *)malloc((size_t)d * sizeof(double));
+        int64_t *locs = (int64_t *)malloc((size_t)d * sizeof(int64_t));
+        int64_t pd[64];
+        if (!raw || !buf || !locs) {
+#pragma omp atomic write
+            failed = 1;
+        } else {
+            for (int64_t r = a; r < b; ++r) {
+                const int64_t row = r * d;
+                for (int64_t s = 0; s < d; ++s) buf[s] = load_count(counts, dtype, row + s) / fshots;
+                wht_inplace(buf, d);
+                place_digits(w_begin + r, n, pd);
+                fill_locations(pd, n, locs);
+                for (int64_t t = 0; t < d; ++t) raw[locs[t]] += buf[t] * scale;
+            }
+        }
+#pragma omp barrier
+        double t2 = omp_get_wtime();
+        if (tid == 0) {
+            t_touch = t1 - t0;
+            t_rows = t2 - t1;
+        }
+        partials[tid] = raw;
+        free(buf);
+        free(locs);
+    }
+    if (failed) {
+        for (int i = 0; i < threads; ++i) free(partials[i]);
+        free(partials);
+        return 1;
+    }
+    double tm0 = omp_get_wtime();
+    for (int i = 1; i < threads; ++i) {
+        double *dst = partials[0];
+        const double *p = partials[i];
+#pragma omp parallel for num_threads(threads) schedule(static)
+        for (int64_t j = 0; j < size; ++j) dst[j] += p[j];
+    }
+    double t_merge = omp_get_wtime() - tm0;
+    for (int i = 0; i < threads; ++i) free(partials[i]);
+    free(partials);
+    *fixed_s = t_touch + t_merge;
+    *per_row_s = t_rows / ((double)total / threads);
+    return 0;
+}
+
 /* Gram diagonal division: theta = raw / 3**zero_count(i) (pipeline.py:138). */
 void lre_oracle_gram_divide(double *theta, int n) {
     const int64_t size = (int64_t)1 << (2 * n);
