@@ -243,6 +243,66 @@ def e2e_host(plan, slabs, n, mu_host, chunk_rows, steps, warmup, torch, lre_dtyp
     return e0.elapsed_time(e1) / 1e3 / steps, wall / steps
 
 
+def e2e_outcomes(plan, st, shots, seed, n, mu_host, chunk_rows, steps, torch):
+    """Same public streaming path, but the host record is an outcome list
+    (2 B per shot, OutcomeRecord): each chunk's outcomes go H2D and are
+    histogrammed into dense counts on the device (lre_counts_from_outcomes)
+    before lre_step1_stage.  Returns (device s/step, wall s/step, h2d bytes,
+    pinned) or raises."""
+    from paper_1602_08604_b200.simulate import generate_device_outcomes
+
+    dev = plan.device
+    rows = 3**n
+    host = []
+    pinned = True
+    for lo in range(0, rows, chunk_rows):
+        hi = min(rows, lo + chunk_rows)
+        o = generate_device_outcomes(st, shots, seed=seed, w_begin=lo, w_end=hi, device=dev)
+        try:
+            h = torch.empty(tuple(o.shape), dtype=torch.uint16, pin_memory=pinned)
+        except Exception:
+            pinned = False
+            h = torch.empty(tuple(o.shape), dtype=torch.uint16)
+        h.copy_(o)
+        host.append((lo, hi, h))
+        del o
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    bufs = [torch.empty((chunk_rows, shots), dtype=torch.uint16, device=dev) for _ in range(2)]
+    ev_copy = [torch.cuda.Event() for _ in range(2)]
+    ev_used = [torch.cuda.Event() for _ in range(2)]
+
+    def one():
+        for k, (lo, hi, h) in enumerate(host):
+            b = k % 2
+            copy.wait_event(ev_used[b])
+            with torch.cuda.stream(copy):
+                bufs[b][: hi - lo].copy_(h, non_blocking=True)
+                ev_copy[b].record(copy)
+            comp.wait_event(ev_copy[b])
+            plan.stage_outcomes(bufs[b][: hi - lo], lo, hi, comp)
+            ev_used[b].record(comp)
+        plan.finish(comp)
+        plan.step2(comp)
+        mu_host.copy_(plan.mu, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    for _ in range(steps):
+        one()
+    e1.record(comp)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    h2d = sum(h.numel() * 2 for _, _, h in host)
+    del bufs, host
+    plan._dense = None
+    return e0.elapsed_time(e1) / 1e3 / steps, wall / steps, h2d, pinned
+
+
 def run_b200(args):
     import torch
 
@@ -350,6 +410,26 @@ def run_b200(args):
                 e2e = {"value": None, "unit": "s", "error": f"{type(exc).__name__}: {str(exc)[:200]}"}
         else:
             e2e = {"value": None, "unit": "s", "skipped": f"host RAM {avail >> 30} GiB < record {host_bytes >> 30} GiB"}
+        # secondary: the same record as raw-shot outcome lists (2 B per shot)
+        try:
+            rec = counts = None
+            torch.cuda.empty_cache()
+            q = int(_lib.load().lre_shard_quantum(n))
+            chunk = max(q, max(1, (2 << 30) // ((1 << n) * c)) // q * q)
+            mu_host = torch.empty(tuple(plan.mu.shape), dtype=plan.mu.dtype, pin_memory=True)
+            ksteps = max(1, min(args.steps, args.e2e_steps))
+            t_o, wall_o, h2d_o, pin_o = e2e_outcomes(plan, st, shots, seed, n, mu_host, chunk, ksteps, torch)
+            e2e_out = {"value": t_o, "unit": "s", "h2d_bytes_per_step": int(h2d_o),
+                       "d2h_bytes_per_step": int(mu_host.numel() * mu_host.element_size()),
+                       "wall_s_per_step": wall_o, "host_memory": "pinned" if pin_o else "pageable", "steps": ksteps,
+                       "api": "OutcomeRecord chunks -> LREPlan.stage_outcomes (lre_counts_from_outcomes + "
+                              "lre_step1_stage) -> finish -> step2",
+                       "same_record": "identical counts (same Philox stream) as the dense record"}
+            del mu_host
+        except Exception as exc:
+            e2e_out = {"value": None, "unit": "s", "error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+        if e2e is not None:
+            e2e["outcome_record"] = e2e_out
 
     # --- step (iii), adjacent to the hot path and timed separately (north star):
     # Hermitian eigensolve (cuSOLVER through torch.linalg.eigh) + simplex projection

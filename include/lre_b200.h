@@ -147,6 +147,22 @@ int lre_generate_counts(int kind, int n, int64_t bits, int64_t shots, uint64_t s
                         int64_t w_begin, int64_t w_end, void *out, int count_dtype,
                         lre_stream_t stream);
 
+/*
+ * Outcome-list records (record ingestion at scale): a
+ * sampled record as the outcome of every shot, outcomes[(w - w_begin) * shots
+ * + k] (uint16, n <= 16) — 2 bytes per shot instead of 2^n counts per setting
+ * (n = 14, 1000 shots: 9.6 GB instead of 157 GB of uint16 counts).
+ * lre_generate_outcomes draws them with the same Philox stream as
+ * lre_generate_counts (so their histogram equals that record);
+ * lre_counts_from_outcomes turns `rows` outcome lists (device) into dense
+ * counts (device, count_dtype) for lre_step1 / lre_step1_stage.  Replaces
+ * the counting inside reference simulate.py:224-242 (sample_counts).
+ */
+int lre_generate_outcomes(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, int64_t w_begin,
+                          int64_t w_end, uint16_t *out, lre_stream_t stream);
+int lre_counts_from_outcomes(const uint16_t *outcomes, int n, int64_t shots, int64_t rows, void *counts,
+                             int count_dtype, lre_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,6 +36,8 @@ _SIGNATURES = {
     "lre_assemble": (_i, [_vp, _i, _i, _i64, _i64, _vp, _vp]),
     "lre_validate_counts": (_i, [_vp, _i, _i, _i64, _i64, _vp, _vp]),
     "lre_generate_counts": (_i, [_i, _i, _i64, _i64, _u64, _i, _i64, _i64, _vp, _i, _vp]),
+    "lre_generate_outcomes": (_i, [_i, _i, _i64, _i64, _u64, _i64, _i64, _vp, _vp]),
+    "lre_counts_from_outcomes": (_i, [_vp, _i, _i64, _i64, _vp, _i, _vp]),
 }
 EXPORTED = tuple(_SIGNATURES)
 

@@ -28,6 +28,10 @@ int finalize_impl(const int64_t *num, int n, int64_t shots, int layout, int64_t 
 int relayout_impl(const double *src, int src_layout, int n, double *dst, cudaStream_t s);
 int generate_impl(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, int exact, int64_t w_begin,
                   int64_t w_end, void *out, int dtype, cudaStream_t s);
+int generate_outcomes_impl(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, int64_t w_begin,
+                           int64_t w_end, uint16_t *out, cudaStream_t s);
+int counts_from_outcomes_impl(const uint16_t *outcomes, int n, int64_t shots, int64_t rows, void *counts, int dtype,
+                              cudaStream_t s);
 }  // namespace lre
 
 static inline int64_t pow3_i(int n) {
@@ -151,6 +155,24 @@ int lre_generate_counts(int kind, int n, int64_t bits, int64_t shots, uint64_t s
     if (kind == LRE_STATE_PRODUCTZ && (bits < 0 || bits >= ((int64_t)1 << n))) return LRE_EINVAL;
     return lre::generate_impl(kind, n, bits, shots, seed, exact, w_begin, w_end, out, count_dtype,
                               reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_generate_outcomes(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, int64_t w_begin,
+                          int64_t w_end, uint16_t *out, lre_stream_t stream) {
+    if (!valid_n(n) || !out || shots < 1) return LRE_EINVAL;
+    if (w_begin < 0 || w_end > pow3_i(n) || w_begin > w_end) return LRE_EINVAL;
+    if (kind == LRE_STATE_PRODUCTZ && (bits < 0 || bits >= ((int64_t)1 << n))) return LRE_EINVAL;
+    return lre::generate_outcomes_impl(kind, n, bits, shots, seed, w_begin, w_end, out,
+                                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_counts_from_outcomes(const uint16_t *outcomes, int n, int64_t shots, int64_t rows, void *counts,
+                             int count_dtype, lre_stream_t stream) {
+    if (!valid_n(n) || !outcomes || !counts || shots < 1 || rows < 0) return LRE_EINVAL;
+    if (dtype_max(count_dtype) < 0) return LRE_EINVAL;
+    if (shots > dtype_max(count_dtype)) return LRE_EOVERFLOW;
+    return lre::counts_from_outcomes_impl(outcomes, n, shots, rows, counts, count_dtype,
+                                          reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

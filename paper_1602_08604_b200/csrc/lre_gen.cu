@@ -89,6 +89,40 @@ __device__ __forceinline__ double chain_step(int kind, int64_t bits, int n, int 
     return 1.0;  // maxmixed
 }
 
+// setting digits of w (qubit 1 first; X=0, Y=1, Z=2)
+__device__ __forceinline__ void setting_axes(int64_t w, int n, int ax[16]) {
+    int64_t x = w;
+    for (int k = n - 1; k >= 0; --k) {
+        ax[k] = (int)(x % 3);
+        x /= 3;
+    }
+}
+
+// One shot of setting w: outcome bits drawn qubit by qubit from the exact
+// conditional probabilities, Philox4x32-10 keyed on (seed), counter (shot,
+// qubit group, w) — the same stream whether counts or outcome lists are made.
+__device__ __forceinline__ uint32_t sample_outcome(int kind, int n, int64_t bits, int64_t shot, int64_t w, uint2 key,
+                                                   const int ax[16]) {
+    Chain ch = chain_init(kind, n);
+    uint32_t s = 0;
+    uint4 rnd = make_uint4(0, 0, 0, 0);
+    for (int j = 0; j < n; ++j) {
+        if ((j & 3) == 0)
+            rnd = Philox::gen(make_uint4((uint32_t)shot, (uint32_t)(j >> 2) | ((uint32_t)(shot >> 32) << 8), (uint32_t)w,
+                                         (uint32_t)(w >> 32)),
+                              key);
+        const uint32_t ru = (j & 3) == 0 ? rnd.x : (j & 3) == 1 ? rnd.y : (j & 3) == 2 ? rnd.z : rnd.w;
+        const double U = ((double)ru + 0.5) * 2.3283064365386963e-10;  // (0,1)
+        Chain c0 = ch, c1 = ch;
+        const double w0 = chain_step(kind, bits, n, j, ax[j], 0, c0);
+        const double w1 = chain_step(kind, bits, n, j, ax[j], 1, c1);
+        const int bit = (U * (w0 + w1) < w0) ? 0 : 1;
+        ch = bit ? c1 : c0;
+        s = (s << 1) | (uint32_t)bit;
+    }
+    return s;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) gen_sampled_kernel(int kind, int n, int64_t bits, int64_t shots, uint64_t seed,
                                                           int64_t w_begin, int64_t w_end, T *__restrict__ out) {
@@ -98,37 +132,53 @@ __global__ void __launch_bounds__(256) gen_sampled_kernel(int kind, int n, int64
     for (int64_t w = w_begin + blockIdx.x; w < w_end; w += gridDim.x) {
         for (int j = threadIdx.x; j < d; j += blockDim.x) hist[j] = 0;
         int ax[16];
-        {
-            int64_t x = w;
-            for (int k = n - 1; k >= 0; --k) {
-                ax[k] = (int)(x % 3);
-                x /= 3;
-            }
-        }
+        setting_axes(w, n, ax);
         __syncthreads();
-        for (int64_t shot = threadIdx.x; shot < shots; shot += blockDim.x) {
-            Chain ch = chain_init(kind, n);
-            uint32_t s = 0;
-            uint4 rnd = make_uint4(0, 0, 0, 0);
-            for (int j = 0; j < n; ++j) {
-                if ((j & 3) == 0)
-                    rnd = Philox::gen(make_uint4((uint32_t)shot, (uint32_t)(j >> 2) | ((uint32_t)(shot >> 32) << 8),
-                                                 (uint32_t)w, (uint32_t)(w >> 32)),
-                                      key);
-                const uint32_t ru = (j & 3) == 0 ? rnd.x : (j & 3) == 1 ? rnd.y : (j & 3) == 2 ? rnd.z : rnd.w;
-                const double U = ((double)ru + 0.5) * 2.3283064365386963e-10;  // (0,1)
-                Chain c0 = ch, c1 = ch;
-                const double w0 = chain_step(kind, bits, n, j, ax[j], 0, c0);
-                const double w1 = chain_step(kind, bits, n, j, ax[j], 1, c1);
-                const int bit = (U * (w0 + w1) < w0) ? 0 : 1;
-                ch = bit ? c1 : c0;
-                s = (s << 1) | (uint32_t)bit;
-            }
-            atomicAdd(&hist[s], 1u);
-        }
+        for (int64_t shot = threadIdx.x; shot < shots; shot += blockDim.x)
+            atomicAdd(&hist[sample_outcome(kind, n, bits, shot, w, key, ax)], 1u);
         __syncthreads();
         T *row = out + (w - w_begin) * (int64_t)d;
         for (int j = threadIdx.x; j < d; j += blockDim.x) row[j] = (T)hist[j];
+        __syncthreads();
+    }
+}
+
+// Outcome-list record: out[(w - w_begin) * shots + shot] = outcome of that shot
+__global__ void __launch_bounds__(256) gen_outcomes_kernel(int kind, int n, int64_t bits, int64_t shots, uint64_t seed,
+                                                           int64_t w_begin, int64_t w_end, uint16_t *__restrict__ out) {
+    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    for (int64_t w = w_begin + blockIdx.x; w < w_end; w += gridDim.x) {
+        int ax[16];
+        setting_axes(w, n, ax);
+        for (int64_t shot = threadIdx.x; shot < shots; shot += blockDim.x)
+            out[(w - w_begin) * shots + shot] = (uint16_t)sample_outcome(kind, n, bits, shot, w, key, ax);
+    }
+}
+
+// Outcome lists -> dense counts (record ingestion for sampled data: the host
+// ships 2 bytes per shot instead of 2^n counts per setting).  One CTA per
+// setting row at a time: shared-memory histogram, then one coalesced row store.
+template <typename T>
+__global__ void __launch_bounds__(512) counts_from_outcomes_kernel(const uint16_t *__restrict__ outcomes, int n,
+                                                                   int64_t shots, int64_t rows, T *__restrict__ out) {
+    extern __shared__ unsigned int hist[];
+    const int d = 1 << n;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        for (int j = threadIdx.x; j < d; j += blockDim.x) hist[j] = 0;
+        __syncthreads();
+        const uint16_t *o = outcomes + r * shots;
+        for (int64_t k = threadIdx.x; k < shots; k += blockDim.x) {
+            const unsigned int s = __ldcs(o + k);
+            if (s < (unsigned)d) atomicAdd(&hist[s], 1u);
+        }
+        __syncthreads();
+        T *row = out + r * (int64_t)d;
+        if constexpr (sizeof(T) == 2) {
+            for (int j = 2 * threadIdx.x; j < d; j += 2 * blockDim.x)
+                __stcs(reinterpret_cast<uint32_t *>(row + j), hist[j] | (hist[j + 1] << 16));
+        } else {
+            for (int j = threadIdx.x; j < d; j += blockDim.x) __stcs(row + j, (T)hist[j]);
+        }
         __syncthreads();
     }
 }
@@ -186,6 +236,47 @@ static int gen_t(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, in
     gen_sampled_kernel<T><<<blocks, 256, smem, s>>>(kind, n, bits, shots, seed, w_begin, w_end, reinterpret_cast<T *>(out));
     count_launch();
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
+}
+
+int generate_outcomes_impl(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, int64_t w_begin,
+                           int64_t w_end, uint16_t *out, cudaStream_t s) {
+    if (n < 1 || n > 16) return LRE_EUNSUPPORTED;
+    if (kind < LRE_STATE_MAXMIXED || kind > LRE_STATE_W || shots < 1) return LRE_EINVAL;
+    const int64_t rows = w_end - w_begin;
+    if (rows <= 0) return LRE_OK;
+    const unsigned blocks = (unsigned)std::min<int64_t>(rows, 148 * 16);
+    gen_outcomes_kernel<<<blocks, 256, 0, s>>>(kind, n, bits, shots, seed, w_begin, w_end, out);
+    count_launch();
+    return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
+}
+
+template <typename T>
+static int hist_t(const uint16_t *outcomes, int n, int64_t shots, int64_t rows, void *counts, cudaStream_t s) {
+    const size_t smem = ((size_t)1 << n) * sizeof(unsigned int);
+    cudaError_t e = cudaFuncSetAttribute(counts_from_outcomes_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return LRE_ECUDA;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = std::max(1, std::min(4, (int)((200 * 1024) / smem)));
+    const unsigned blocks = (unsigned)std::min<int64_t>(rows, (int64_t)sms * per_sm);
+    counts_from_outcomes_kernel<T><<<blocks, 512, smem, s>>>(outcomes, n, shots, rows, reinterpret_cast<T *>(counts));
+    count_launch();
+    return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
+}
+
+int counts_from_outcomes_impl(const uint16_t *outcomes, int n, int64_t shots, int64_t rows, void *counts, int dtype,
+                              cudaStream_t s) {
+    if (n < 1 || n > 16) return LRE_EUNSUPPORTED;
+    if (rows <= 0) return LRE_OK;
+    switch (dtype) {
+    case LRE_U8: return hist_t<uint8_t>(outcomes, n, shots, rows, counts, s);
+    case LRE_U16: return hist_t<uint16_t>(outcomes, n, shots, rows, counts, s);
+    case LRE_I32: return hist_t<int32_t>(outcomes, n, shots, rows, counts, s);
+    case LRE_I64: return hist_t<int64_t>(outcomes, n, shots, rows, counts, s);
+    default: return LRE_EINVAL;
+    }
 }
 
 int generate_impl(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, int exact, int64_t w_begin,

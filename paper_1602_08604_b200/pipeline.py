@@ -29,7 +29,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib, pauli
-from .records import DeviceRecord, MeasurementRecord, lre_dtype_of
+from .records import DeviceRecord, MeasurementRecord, OutcomeRecord, compact_dtype, lre_dtype_of
 from .simulate import StateDescriptor, exact_record
 
 KERNELS = ("b200", "fast", "paper-direct")
@@ -74,6 +74,18 @@ def to_device_record(record_or_source, device=None, stream=None) -> DeviceRecord
                 "integer counts, sample a record with simulate.sample_counts instead"
             )
         return exact_record(record_or_source, device=dev).validate(stream)
+    if isinstance(record_or_source, OutcomeRecord):
+        rec = record_or_source
+        n = pauli.check_qubit_count(rec.n)
+        o = rec.outcomes
+        if not isinstance(o, torch.Tensor):
+            o = torch.from_numpy(np.ascontiguousarray(np.asarray(o, dtype=np.uint16)))
+        o = o.to(dev, non_blocking=False)
+        if o.dim() != 2 or int(o.shape[1]) != int(rec.shots) or o.dtype != torch.uint16:
+            raise ValueError(f"outcomes must be uint16 of shape (settings, shots={rec.shots}), got {tuple(o.shape)}")
+        counts = counts_from_outcomes(o, n, int(rec.shots), stream=stream)
+        return DeviceRecord(n=n, shots=int(rec.shots), counts=counts, w_begin=rec.w_begin, seed=rec.seed,
+                            state=rec.state).validate(stream)
     if isinstance(record_or_source, MeasurementRecord):
         rec = record_or_source
         n = pauli.check_qubit_count(rec.n)
@@ -94,6 +106,20 @@ def to_device_record(record_or_source, device=None, stream=None) -> DeviceRecord
         f"unsupported source {type(record_or_source).__name__}: pass a MeasurementRecord, DeviceRecord "
         "or StateDescriptor"
     )
+
+
+def counts_from_outcomes(outcomes, n: int, shots: int, out=None, stream=None):
+    """Device outcome lists (uint16, rows x shots) -> dense device counts (lre_counts_from_outcomes)."""
+    torch = _torch()
+    rows = int(outcomes.shape[0])
+    if out is None:
+        dt = {np.uint8: torch.uint8, np.uint16: torch.uint16, np.int32: torch.int32,
+              np.int64: torch.int64}[compact_dtype(shots)]
+        out = torch.empty((rows, 1 << n), dtype=dt, device=outcomes.device)
+    stream = stream if stream is not None else torch.cuda.current_stream(outcomes.device)
+    _lib.call("lre_counts_from_outcomes", outcomes.data_ptr(), n, int(shots), rows, out.data_ptr(),
+              lre_dtype_of(out.dtype), stream.cuda_stream)
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -138,6 +164,19 @@ class LREPlan:
     def stage(self, chunk, count_dtype: int, w_begin: int, w_end: int, stream) -> None:
         _lib.call("lre_step1_stage", chunk.data_ptr(), count_dtype, self.n, self.shots, int(w_begin), int(w_end),
                   self.ws.data_ptr(), self.ws_bytes, stream.cuda_stream)
+
+    def stage_outcomes(self, outcomes, w_begin: int, w_end: int, stream) -> None:
+        """Streaming ingestion of an outcome-list chunk: histogram on the device, then stage."""
+        torch = _torch()
+        rows = int(outcomes.shape[0])
+        buf = getattr(self, "_dense", None)
+        if buf is None or buf.shape[0] < rows:
+            dt = {np.uint8: torch.uint8, np.uint16: torch.uint16, np.int32: torch.int32,
+                  np.int64: torch.int64}[compact_dtype(self.shots)]
+            self._dense = buf = torch.empty((rows, 1 << self.n), dtype=dt, device=self.device)
+        dense = buf[:rows]
+        counts_from_outcomes(outcomes, self.n, self.shots, out=dense, stream=stream)
+        self.stage(dense, lre_dtype_of(dense.dtype), w_begin, w_end, stream)
 
     def finish(self, stream) -> None:
         _lib.call("lre_step1_finish", self.ws.data_ptr(), self.ws_bytes, self.n, self.shots,

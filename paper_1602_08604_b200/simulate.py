@@ -120,3 +120,30 @@ def exact_record(state: StateDescriptor, dtype=None, device=None) -> DeviceRecor
 
 def to_host_record(rec: DeviceRecord) -> MeasurementRecord:
     return rec.to_host()
+
+
+def generate_device_outcomes(state: StateDescriptor, shots: int, seed: int = 0, w_begin: int = 0,
+                             w_end: int | None = None, device=None, out=None, stream=None):
+    """Outcome lists of settings [w_begin, w_end) on the device (uint16, rows x shots), drawn
+    with the same Philox stream as generate_device_counts (their histogram is that record)."""
+    import torch
+
+    n = state.n
+    w_end = 3**n if w_end is None else int(w_end)
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if out is None:
+        out = torch.empty((w_end - w_begin, int(shots)), dtype=torch.uint16, device=device)
+    stream = stream if stream is not None else torch.cuda.current_stream(device)
+    _lib.call("lre_generate_outcomes", _lib.STATE_KINDS[state.kind], n, int(state.bits), int(shots),
+              int(seed) & 0xFFFFFFFFFFFFFFFF, int(w_begin), int(w_end), out.data_ptr(), stream.cuda_stream)
+    return out
+
+
+def sample_outcomes(state: StateDescriptor, shots: int, seed: int, device=None):
+    """OutcomeRecord drawn on the device (the raw-shot form of sample_counts)."""
+    from .records import OutcomeRecord
+
+    if shots < 1:
+        raise ValueError(f"shots must be >= 1, got {shots}")
+    outcomes = generate_device_outcomes(state, shots, seed=seed, device=device)
+    return OutcomeRecord(n=state.n, shots=shots, outcomes=outcomes, seed=seed, state=state.label())

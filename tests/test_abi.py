@@ -73,3 +73,18 @@ def test_argument_errors_map_to_reference_exceptions():
         _lib.check(_lib.LRE_EUNSUPPORTED, "x")
     with pytest.raises(RuntimeError):
         _lib.check(_lib.LRE_ECUDA, "x")
+
+
+def test_outcome_record_host_histogram():
+    """OutcomeRecord.to_counts: the host restatement of lre_counts_from_outcomes."""
+    import numpy as np
+    from paper_1602_08604_b200.records import OutcomeRecord
+
+    rng = np.random.default_rng(0)
+    n, shots = 3, 50
+    o = rng.integers(0, 8, size=(27, shots), dtype=np.uint16)
+    rec = OutcomeRecord(n=n, shots=shots, outcomes=o).to_counts()
+    assert rec.counts.shape == (27, 8) and rec.counts.dtype == np.uint8
+    assert (rec.counts.sum(axis=1) == shots).all()
+    for w in (0, 13, 26):
+        np.testing.assert_array_equal(rec.counts[w], np.bincount(o[w], minlength=8))
