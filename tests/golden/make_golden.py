@@ -22,6 +22,13 @@ Cases:
                    tests regenerate the counts with the oracle's restatement
                    of simulate.sample_counts and check the hash first.
   validate.npz     MeasurementRecord.validate error messages.
+  files/           file formats written by the reference itself: a
+                   pauli-lre/1 text record (records.py:67-84), a PLRE v1
+                   state file (statefile.py:19-29), and the messages its
+                   readers raise on the perturbations tests/test_recordio.py
+                   applies (files/messages.json).
+
+Run a subset with `python tests/golden/make_golden.py files`.
 """
 
 from __future__ import annotations
@@ -45,6 +52,7 @@ from pauli_lre import pauli, pipeline, simulate  # noqa: E402  (the reference)
 from pauli_lre.records import MeasurementRecord  # noqa: E402
 
 from oracle import lre_oracle as O  # noqa: E402
+from perturb import record_perturbations, state_perturbations  # noqa: E402
 
 SEED = 1602
 
@@ -190,11 +198,47 @@ def validate_messages():
     _save("validate.npz", counts_bad_row=counts, counts_ok=ok, messages=np.array(json.dumps(msgs)))
 
 
+def files():
+    from pauli_lre import records, statefile
+
+    d = os.path.join(HERE, "files")
+    os.makedirs(d, exist_ok=True)
+    st = simulate.parse_state("ghz", 2)
+    rec = simulate.sample_counts(st, 50, seed=SEED)
+    records.write_record(rec, os.path.join(d, "record_ghz2.txt"))
+    st3 = simulate.parse_state("random:8604", 3)
+    rec3 = simulate.sample_counts(st3, 200, seed=SEED)
+    records.write_record(rec3, os.path.join(d, "record_random3.txt"))
+    rho = pipeline.reconstruct(rec3, workers=1).rho
+    statefile.write_state(os.path.join(d, "state_random3.plre"), rho)
+    msgs = {}
+    lines = open(os.path.join(d, "record_ghz2.txt")).read().splitlines()
+    tmp = tempfile.mkdtemp()
+    for name, L in record_perturbations(lines).items():
+        path = os.path.join(tmp, name + ".txt")
+        with open(path, "w") as fh:
+            fh.write("\n".join(L) + ("\n" if L else ""))
+        try:
+            records.read_record(path)
+            msgs["record:" + name] = None
+        except records.RecordFormatError as exc:
+            msgs["record:" + name] = str(exc)
+    blob = open(os.path.join(d, "state_random3.plre"), "rb").read()
+    for name, b in state_perturbations(blob).items():
+        path = os.path.join(tmp, "state.plre")
+        with open(path, "wb") as fh:
+            fh.write(b)
+        try:
+            statefile.read_state(path)
+            msgs["state:" + name] = None
+        except ValueError as exc:
+            msgs["state:" + name] = str(exc).replace(path, "<path>")
+    with open(os.path.join(d, "messages.json"), "w") as fh:
+        json.dump(msgs, fh, indent=1, sort_keys=True)
+    print("wrote files/ (", ", ".join(sorted(os.listdir(d))), ")")
+
+
 if __name__ == "__main__":
-    kat()
-    blocks()
-    c1()
-    small()
-    validate_messages()
-    c2()
-    c3()
+    todo = sys.argv[1:] or ["kat", "blocks", "c1", "small", "validate_messages", "c2", "c3", "files"]
+    for name in todo:
+        globals()[name]()
