@@ -163,6 +163,34 @@ int lre_generate_outcomes(int kind, int n, int64_t bits, int64_t shots, uint64_t
 int lre_counts_from_outcomes(const uint16_t *outcomes, int n, int64_t shots, int64_t rows, void *counts,
                              int count_dtype, lre_stream_t stream);
 
+/*
+ * Error metrics on the device (reference metrics.py).
+ *
+ * lre_reduce: deterministic fp64 reduction of `count` doubles (device) into
+ * out[0]; out (device) must hold 1 + LRE_REDUCE_BLOCKS doubles (out[1..] is
+ * scratch).  Bit-reproducible for a given count (fixed grid, fixed order).
+ *   LRE_REDUCE_SUM_SQ     sum (a_i - b_i)^2, b may be NULL: squared Hilbert-
+ *                         Schmidt distance over a complex matrix viewed as
+ *                         2 d^2 doubles (replaces metrics.py:28-35)
+ *   LRE_REDUCE_SUM_SQRT   sum sqrt(max(a_i, 0) * scale): with scale = 1/d over
+ *                         a spectrum, sqrt of the fidelity with I/d
+ *                         (replaces metrics.py:88-92)
+ *   LRE_REDUCE_SUM_SQ_ZC  sum 3^zc(i) a_i^2 over a NATURAL theta (count = 4^n,
+ *                         zc = identity digits of i) = sum over settings and
+ *                         outcomes of p_ws^2 (the dense MSE predictor,
+ *                         metrics.py:124-154, in closed form)
+ * lre_truth_terms: for the generator's states, out[0] = Re Tr(A rho_true) and
+ * out[1] = Tr(rho_true^2), A a row-major 2^n x 2^n complex128 Hermitian
+ * matrix (device); squared HS distance to the truth is
+ * ||A||^2 - 2 out[0] + out[1], and for a pure truth out[0] is the fidelity
+ * <psi|A|psi> (metrics.py:57-85, evaluate_errors :173-201).
+ */
+#define LRE_REDUCE_BLOCKS 1184
+enum { LRE_REDUCE_SUM_SQ = 0, LRE_REDUCE_SUM_SQRT = 1, LRE_REDUCE_SUM_SQ_ZC = 2 };
+int lre_reduce(int op, const double *a, const double *b, int64_t count, double scale, double *out,
+               lre_stream_t stream);
+int lre_truth_terms(const double *a, int n, int kind, int64_t bits, double *out, lre_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

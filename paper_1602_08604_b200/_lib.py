@@ -18,6 +18,8 @@ U8, U16, I32, I64 = 1, 2, 3, 4
 NATURAL, MASK_MAJOR = 0, 1
 OUT_THETA_F64, OUT_NUM_I64 = 0, 1
 STATE_KINDS = {"maxmixed": 0, "ghz": 1, "productz": 2, "w": 3}
+REDUCE_BLOCKS = 1184  # LRE_REDUCE_BLOCKS
+REDUCE_SUM_SQ, REDUCE_SUM_SQRT, REDUCE_SUM_SQ_ZC = 0, 1, 2
 
 # name -> (restype, argtypes)
 _i64, _i, _vp, _sz, _u64 = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64
@@ -38,6 +40,8 @@ _SIGNATURES = {
     "lre_generate_counts": (_i, [_i, _i, _i64, _i64, _u64, _i, _i64, _i64, _vp, _i, _vp]),
     "lre_generate_outcomes": (_i, [_i, _i, _i64, _i64, _u64, _i64, _i64, _vp, _vp]),
     "lre_counts_from_outcomes": (_i, [_vp, _i, _i64, _i64, _vp, _i, _vp]),
+    "lre_reduce": (_i, [_i, _vp, _vp, _i64, ctypes.c_double, _vp, _vp]),
+    "lre_truth_terms": (_i, [_vp, _i, _i, _i64, _vp, _vp]),
 }
 EXPORTED = tuple(_SIGNATURES)
 

@@ -32,6 +32,8 @@ int generate_outcomes_impl(int kind, int n, int64_t bits, int64_t shots, uint64_
                            int64_t w_end, uint16_t *out, cudaStream_t s);
 int counts_from_outcomes_impl(const uint16_t *outcomes, int n, int64_t shots, int64_t rows, void *counts, int dtype,
                               cudaStream_t s);
+int reduce_impl(int op, const double *a, const double *b, int64_t count, double scale, double *out, cudaStream_t s);
+int truth_terms_impl(const double *a, int n, int kind, int64_t bits, double *out, cudaStream_t s);
 }  // namespace lre
 
 static inline int64_t pow3_i(int n) {
@@ -173,6 +175,20 @@ int lre_counts_from_outcomes(const uint16_t *outcomes, int n, int64_t shots, int
     if (shots > dtype_max(count_dtype)) return LRE_EOVERFLOW;
     return lre::counts_from_outcomes_impl(outcomes, n, shots, rows, counts, count_dtype,
                                           reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_reduce(int op, const double *a, const double *b, int64_t count, double scale, double *out,
+               lre_stream_t stream) {
+    if (!a || !out || count < 0) return LRE_EINVAL;
+    if (op < LRE_REDUCE_SUM_SQ || op > LRE_REDUCE_SUM_SQ_ZC) return LRE_EINVAL;
+    return lre::reduce_impl(op, a, b, count, scale, out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_truth_terms(const double *a, int n, int kind, int64_t bits, double *out, lre_stream_t stream) {
+    if (!valid_n(n) || !a || !out) return LRE_EINVAL;
+    if (kind < LRE_STATE_MAXMIXED || kind > LRE_STATE_W) return LRE_EINVAL;
+    if (kind == LRE_STATE_PRODUCTZ && (bits < 0 || bits >= ((int64_t)1 << n))) return LRE_EINVAL;
+    return lre::truth_terms_impl(a, n, kind, bits, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -39,6 +39,13 @@ _HERMITIAN_TOL = 1e-10  # pipeline.py:36
 _TRACE_TOL = 1e-8  # pipeline.py:37
 
 
+_NP_TO_TORCH = {"uint8": "uint8", "uint16": "uint16", "int32": "int32", "int64": "int64"}
+
+
+def _torch_count_dtype(np_dtype):
+    return getattr(_torch(), _NP_TO_TORCH[np.dtype(np_dtype).name])
+
+
 def _torch():
     import torch
 
@@ -113,9 +120,7 @@ def counts_from_outcomes(outcomes, n: int, shots: int, out=None, stream=None):
     torch = _torch()
     rows = int(outcomes.shape[0])
     if out is None:
-        dt = {np.uint8: torch.uint8, np.uint16: torch.uint16, np.int32: torch.int32,
-              np.int64: torch.int64}[compact_dtype(shots)]
-        out = torch.empty((rows, 1 << n), dtype=dt, device=outcomes.device)
+        out = torch.empty((rows, 1 << n), dtype=_torch_count_dtype(compact_dtype(shots)), device=outcomes.device)
     stream = stream if stream is not None else torch.cuda.current_stream(outcomes.device)
     _lib.call("lre_counts_from_outcomes", outcomes.data_ptr(), n, int(shots), rows, out.data_ptr(),
               lre_dtype_of(out.dtype), stream.cuda_stream)
@@ -171,8 +176,7 @@ class LREPlan:
         rows = int(outcomes.shape[0])
         buf = getattr(self, "_dense", None)
         if buf is None or buf.shape[0] < rows:
-            dt = {np.uint8: torch.uint8, np.uint16: torch.uint16, np.int32: torch.int32,
-                  np.int64: torch.int64}[compact_dtype(self.shots)]
+            dt = _torch_count_dtype(compact_dtype(self.shots))
             self._dense = buf = torch.empty((rows, 1 << self.n), dtype=dt, device=self.device)
         dense = buf[:rows]
         counts_from_outcomes(outcomes, self.n, self.shots, out=dense, stream=stream)
@@ -346,6 +350,53 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
         "gpus": 1,
     }
     mu = plan.mu
+    if not as_tensor:
+        same = rho is mu
+        theta, mu = theta.cpu().numpy(), mu.cpu().numpy()
+        rho = mu if same else rho.cpu().numpy()
+        evals = None if evals is None else evals.cpu().numpy()
+    return ReconstructionResult(theta=theta, mu=mu, rho=rho, eigenvalues=evals, timings=timings)
+
+
+def reconstruct_generated(state: StateDescriptor, shots: int, seed: int, *, device=None, project: bool = True,
+                          chunk_bytes: int = 1 << 31, as_tensor: bool = True) -> ReconstructionResult:
+    """Sample a record with the device generator and reconstruct it, chunk by
+    chunk: each setting chunk (a multiple of lre_shard_quantum) is generated
+    into one reusable HBM buffer and folded by the first pass
+    (lre_step1_stage), so the record is never resident — n = 14 with
+    int32 counts (d*N0 shots per setting, 313 GB) needs only the chunk.  The
+    counts are identical to sample_counts(state, shots, seed)."""
+    torch = _torch()
+    from .simulate import generate_device_counts
+
+    n = pauli.check_qubit_count(state.n)
+    dev = _device(device)
+    plan = LREPlan(n, shots, dev)
+    stream = torch.cuda.current_stream(dev)
+    q = int(_lib.load().lre_shard_quantum(n))
+    dt = compact_dtype(shots)
+    row_bytes = (1 << n) * np.dtype(dt).itemsize
+    chunk = max(q, (max(1, chunk_bytes // row_bytes)) // q * q)
+    buf = torch.empty((min(chunk, 3**n), 1 << n), dtype=_torch_count_dtype(dt), device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record(stream)
+    for lo in range(0, 3**n, chunk):
+        hi = min(3**n, lo + chunk)
+        block = buf[: hi - lo]
+        generate_device_counts(state, shots, seed=seed, w_begin=lo, w_end=hi, out=block, stream=stream)
+        plan.stage(block, lre_dtype_of(block.dtype), lo, hi, stream)
+    plan.finish(stream)
+    del buf
+    ev[1].record(stream)
+    plan.step2(stream)
+    ev[2].record(stream)
+    rho, evals = step_three_project(plan.mu) if project else (plan.mu, None)
+    ev[3].record(stream)
+    ev[3].synchronize()
+    t1, t2, t3 = (ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(3))
+    timings = {"t_generate_and_step1_s": t1, "t_step2_s": t2, "t_step3_s": t3, "t_total_s": t1 + t2 + t3,
+               "threads": 1, "kernel": "b200", "gpus": 1}
+    theta, mu = plan.theta, plan.mu
     if not as_tensor:
         same = rho is mu
         theta, mu = theta.cpu().numpy(), mu.cpu().numpy()

@@ -28,6 +28,11 @@ Cases:
                    readers raise on the perturbations tests/test_recordio.py
                    applies (files/messages.json).
 
+  metrics.npz      reference metrics.py on reference reconstructions:
+                   evaluate_errors reports (ghz4 sampled, maxmixed4 sampled,
+                   productz3 sampled), predicted_mse_dense for dense states
+                   n <= 4, fidelity (auto and general) on random pairs.
+
 Run a subset with `python tests/golden/make_golden.py files`.
 """
 
@@ -238,7 +243,46 @@ def files():
     print("wrote files/ (", ", ".join(sorted(os.listdir(d))), ")")
 
 
+def metrics_cases():
+    from pauli_lre import metrics
+
+    out = {}
+    reports = {}
+    cases = [("ghz4", simulate.StateDescriptor("ghz", 4), 16 * 60, 31),
+             ("maxmixed4", simulate.StateDescriptor("maxmixed", 4), 16 * 40, 32),
+             ("productz3", simulate.StateDescriptor("productz", 3, bits=0b101), 8 * 50, 33)]
+    for name, st, shots, seed in cases:
+        rec = simulate.sample_counts(st, shots=shots, seed=seed)
+        res = pipeline.reconstruct(rec, workers=1)
+        d = 1 << st.n
+        rep = metrics.evaluate_errors(st, res.rho, res.mu, n0=shots / d)
+        out[f"{name}_mu"] = res.mu
+        out[f"{name}_rho"] = res.rho
+        reports[name] = json.loads(rep.to_json())
+        reports[name]["shots"] = shots
+    preds = {}
+    for label, st in [("ghz3", simulate.StateDescriptor("ghz", 3)), ("productz2", simulate.StateDescriptor(
+            "productz", 2, bits=2)), ("maxmixed4", simulate.StateDescriptor("maxmixed", 4)),
+            ("random3", simulate.StateDescriptor("random", 3, state_seed=9)),
+            ("random4", simulate.StateDescriptor("random", 4, state_seed=10))]:
+        rho = simulate.dense_matrix(st)
+        out[f"pred_{label}_rho"] = rho
+        preds[label] = metrics.predicted_mse_dense(rho, 37.0)
+    fids = {}
+    for k, (a, b) in enumerate([(5, 6), (7, 8)]):
+        ra = simulate.dense_matrix(simulate.StateDescriptor("random", 3, state_seed=a))
+        rb = simulate.dense_matrix(simulate.StateDescriptor("random", 3, state_seed=b))
+        out[f"fid{k}_a"], out[f"fid{k}_b"] = ra, rb
+        fids[f"fid{k}"] = metrics.fidelity(ra, rb, method="general")
+    lam = np.array([0.5, 0.3, 0.2, 0.0, -0.01, 0.01, 0.0, 0.0])
+    fids["maxmixed_spectrum"] = metrics.fidelity_with_maxmixed(lam, 8)
+    out["maxmixed_spectrum"] = lam
+    _save("metrics.npz", reports=np.array(json.dumps(reports)), preds=np.array(json.dumps(preds)),
+          fids=np.array(json.dumps(fids)), **out)
+
+
 if __name__ == "__main__":
-    todo = sys.argv[1:] or ["kat", "blocks", "c1", "small", "validate_messages", "c2", "c3", "files"]
+    todo = sys.argv[1:] or ["kat", "blocks", "c1", "small", "validate_messages", "c2", "c3", "files",
+                            "metrics_cases"]
     for name in todo:
         globals()[name]()
