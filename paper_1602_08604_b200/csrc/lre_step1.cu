@@ -905,6 +905,7 @@ struct VArgs {
     int64_t xa0, alo, ahi;
     int64_t A0, nA, ya0;
     int64_t nB;  // 2^(R-Q)
+    int vf1_batch;  // Q = 1: issue all row loads of 4 elements first (LRE_VF1=0 disables; A/B only)
     Final f;
 };
 
@@ -989,6 +990,52 @@ __global__ void __launch_bounds__(128, 4) vfold_kernel(const VArgs a) {
     constexpr int RL = R3 / 3;  // rows per top digit
     const int64_t total = a.nA * a.nB * a.V;
     const Tin *in = reinterpret_cast<const Tin *>(a.in);
+    if (Q == 1 && a.vf1_batch) {
+        // One qubit: each thread issues the six row loads of VF1_U elements
+        // before any arithmetic (the r1-streamed vblock keeps only two loads
+        // in flight, which held the final n = 14 pass at 2.4 TB/s).
+        constexpr int U = 4;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < total; t0 += U * stride) {
+            Ta x[U][6];
+            int64_t vv[U], AA[U], BB[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t t = t0 + u * stride;
+                const int64_t V = opaque(a.V);
+                vv[u] = t % V;
+                const int64_t rest = t / V;
+                BB[u] = rest % a.nB;
+                AA[u] = a.A0 + rest / a.nB;
+                const int64_t row0 = AA[u] * 3;
+                const Tin *p0 = in + ((row0 - a.xa0) * a.ncol + BB[u] * 2) * V + vv[u];
+                const int64_t rstride = a.ncol * V;
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                    for (int b = 0; b < 2; ++b) {
+                        const int64_t row = row0 + r;
+                        x[u][2 * r + b] = (t < total && row >= a.alo && row < a.ahi)
+                                              ? (Ta)vload<Tin>(p0 + r * rstride + b * V)
+                                              : (Ta)0;
+                    }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (t0 + u * stride >= total) break;
+                const Ta I = (x[u][0] + x[u][1]) + (x[u][2] + x[u][3]) + (x[u][4] + x[u][5]);
+                const Ta D[4] = {I, x[u][0] - x[u][1], x[u][2] - x[u][3], x[u][4] - x[u][5]};
+                if constexpr (!FINAL) {
+                    Ta *out = reinterpret_cast<Ta *>(a.f.out) + ((AA[u] - a.ya0) * a.nB + BB[u]) * 4 * a.V + vv[u];
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) out[(int64_t)d * a.V] = D[d];
+                } else {
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) store_final(a.f, (uint64_t)(d * a.V + vv[u]), (int64_t)D[d]);
+                }
+            }
+        }
+    } else {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t V = opaque(a.V);
         const int64_t v = t % V;
@@ -1010,6 +1057,7 @@ __global__ void __launch_bounds__(128, 4) vfold_kernel(const VArgs a) {
         } else {
             vblock<Q, Ta>(ld, [&](int d, Ta y) { store_final(a.f, (uint64_t)(d * V + v), (int64_t)y); });
         }
+    }
     }
 }
 
@@ -1509,6 +1557,11 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             a.nA = ps.nA;
             a.ya0 = fin ? 0 : ls.A0;
             a.nB = ipow(2, R - ps.q);
+            static const int vf1 = [] {
+                const char *v = getenv("LRE_VF1");
+                return v && v[0] == '0' ? 0 : 1;
+            }();
+            a.vf1_batch = vf1;
             a.f = f;
             e = run_vfold(ps.q, ps.in_dtype, ps.acc64, a, stream);
         }

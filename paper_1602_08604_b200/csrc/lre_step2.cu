@@ -24,6 +24,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <cmath>
 
 #include "lre_internal.cuh"
@@ -33,6 +36,26 @@ namespace lre {
 namespace cg = cooperative_groups;
 
 __device__ __forceinline__ int padix(int i) { return i + (i >> 4); }
+
+// 256-bit global accesses (sm_100): one transaction per 32-byte run / row segment
+__device__ __forceinline__ void st256_cs(double2 *dst, double2 v0, double2 v1) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(v0.x), "d"(v0.y), "d"(v1.x), "d"(v1.y)
+                 : "memory");
+}
+__device__ __forceinline__ double4 ld256_nc(const double *src) {
+    double4 v;
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(src));
+    return v;
+}
+
+// Cluster barrier without release/acquire semantics: the end-of-iteration
+// barrier only has to order the partners' DSMEM reads (already consumed by
+// their stores) before this CTA overwrites its buffer.  cluster.sync()'s
+// release would also wait for this thread's streaming global stores to
+// drain (the "membar" stall in the n = 14 profile).
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 
 template <int NB>
 __device__ __forceinline__ void wht_round(double *buf, int Dp, int logd, int nm, int shift) {
@@ -120,7 +143,7 @@ __device__ __forceinline__ void asm_load(const AsmArgs &a, double *sbuf, int Dp,
     }
 }
 
-__global__ void __launch_bounds__(1024, 1) assemble_kernel(const AsmArgs a) {
+__global__ void __launch_bounds__(1024) assemble_kernel(const AsmArgs a) {
     extern __shared__ double sbuf[];
     const int d = 1 << a.logd;
     const int Dp = d + (d >> 4) + 1;
@@ -132,6 +155,24 @@ __global__ void __launch_bounds__(1024, 1) assemble_kernel(const AsmArgs a) {
         __syncthreads();
         wht_all(sbuf, Dp, a.logd, B);
         // rows of mu as runs of B adjacent complex values
+        if (B >= 2) {  // aligned mask pairs -> one 32-byte store per (row, pair)
+            const int lp = a.logb - 1;
+            for (int e = threadIdx.x; e < (B >> 1) * d; e += blockDim.x) {
+                const int mp = e & ((B >> 1) - 1), r = e >> lp;
+                const uint32_t m0 = (uint32_t)(a.m_begin + mloc0 + 2 * mp), m1 = m0 + 1;
+                const double *b0 = sbuf + (2 * mp) * Dp, *b1 = b0 + Dp;
+                const double f01 = b0[padix(r)], f02 = b0[padix(r ^ (int)m0)];
+                const double f11 = b1[padix(r)], f12 = b1[padix(r ^ (int)m1)];
+                const double2 v0 = make_double2(a.scale_half * (f01 + f02), a.scale_half * (f02 - f01));
+                const double2 v1 = make_double2(a.scale_half * (f11 + f12), a.scale_half * (f12 - f11));
+                const int64_t c0 = (int64_t)((r ^ m0) & (uint32_t)(S - 1));
+                double2 *dst = a.mu + (int64_t)r * S + (c0 & ~(int64_t)1);
+                if (c0 & 1) st256_cs(dst, v1, v0);
+                else st256_cs(dst, v0, v1);
+            }
+            __syncthreads();
+            continue;
+        }
         for (int e = threadIdx.x; e < B * d; e += blockDim.x) {
             const int ml = e & (B - 1), r = e >> a.logb;
             const uint32_t m = (uint32_t)(a.m_begin + mloc0 + ml);
@@ -147,7 +188,8 @@ __global__ void __launch_bounds__(1024, 1) assemble_kernel(const AsmArgs a) {
 // n >= 13: a cluster of two CTAs transforms the aligned mask pair (m0, m0 + 1);
 // CTA k writes rows [k d/2, (k+1) d/2) of both masks, reading the partner's
 // transform through distributed shared memory -> 32-byte row segments.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) assemble_pair_kernel(const AsmArgs a) {
+template <int NT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) assemble_pair_kernel(const AsmArgs a) {
     extern __shared__ double sbuf[];
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
@@ -179,9 +221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) assemble_pai
                     const int ah = rank * half + base + u * blockDim.x;
                     if (base + u * (int)blockDim.x < half) {
                         const uint64_t run = ma_to_natural(mh, (uint32_t)ah);  // natural index / 4
-                        const double2 *p = reinterpret_cast<const double2 *>(a.theta + 4 * run);
-                        const double2 lo = __ldg(p), hi = __ldg(p + 1);
-                        q[u] = make_double4(lo.x, lo.y, hi.x, hi.y);
+                        q[u] = ld256_nc(a.theta + 4 * run);
                     }
                 }
 #pragma unroll
@@ -217,15 +257,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) assemble_pai
             const double2 v1 = make_double2(a.scale_half * (f11 + f12), a.scale_half * (f12 - f11));
             const int64_t c0 = (int64_t)((r ^ m0) & (uint32_t)(S - 1));  // c0 ^ 1 is mask m1's column
             double2 *dst = a.mu + (int64_t)r * S + (c0 & ~(int64_t)1);
-            if (c0 & 1) {
-                __stcs(dst, v1);
-                __stcs(dst + 1, v0);
-            } else {
-                __stcs(dst, v0);
-                __stcs(dst + 1, v1);
-            }
+            if (c0 & 1) st256_cs(dst, v1, v0);
+            else st256_cs(dst, v0, v1);
         }
-        cluster.sync();  // the partner has finished reading this CTA's transform
+        cluster_sync_relaxed();  // the partner has finished reading this CTA's transform
     }
 }
 
@@ -241,7 +276,10 @@ int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int Dp = (int)(d + (d >> 4) + 1);
-    const size_t smem_budget = 150 * 1024;
+    static const size_t smem_budget = [] {
+        const char *v = getenv("LRE_ASM_BUDGET_KB");  // A/B experiments only
+        return (size_t)(v ? atoi(v) : 150) * 1024;
+    }();
     int logb = 0;
     while (logb < 3 && ((int64_t)2 << logb) <= S && (size_t)(2 << logb) * Dp * sizeof(double) <= smem_budget) ++logb;
     AsmArgs a;
@@ -259,16 +297,20 @@ int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64
     if (logb == 0 && S >= 2) {
         a.cl = 2;
         a.groups = S / 2;
-        e = cudaFuncSetAttribute(assemble_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(assemble_pair_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return LRE_ECUDA;
-        const int64_t grid = 2 * std::min<int64_t>(a.groups, num_sms / 2);
-        assemble_pair_kernel<<<(unsigned)grid, 512, smem, s>>>(a);
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, assemble_pair_kernel<512>, 512, smem);
+        const int64_t grid = 2 * std::min<int64_t>(a.groups, (int64_t)num_sms * std::max(1, per_sm) / 2);
+        assemble_pair_kernel<512><<<(unsigned)grid, 512, smem, s>>>(a);
     } else {
         a.cl = 1;
         a.groups = S >> logb;
         e = cudaFuncSetAttribute(assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return LRE_ECUDA;
-        const int64_t grid = std::min<int64_t>(a.groups, (int64_t)num_sms * (smem <= 110 * 1024 ? 2 : 1));
+        int per_sm = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, assemble_kernel, threads, smem);
+        const int64_t grid = std::min<int64_t>(a.groups, (int64_t)num_sms * std::max(1, per_sm));
         assemble_kernel<<<(unsigned)grid, threads, smem, s>>>(a);
     }
     count_launch();
