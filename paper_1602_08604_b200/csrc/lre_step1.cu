@@ -119,6 +119,7 @@ struct P1Args {
     int64_t naH;         // number of tile row groups computed
     int64_t out_aH0;     // first tile row group held by the output buffer
     int64_t C;           // column tiles, 2^(n-Q)
+    int logC;            // log2(C): tile index math by shifts
     Final f;             // f.kind == OUT_INTER: Y1 int32 tile-major
     int debug_no_l2;     // diagnostics only (LRE_P1_DEBUG=noL2 / noL1): skip L2 / L1 work, output invalid
     int debug_no_l1;
@@ -358,8 +359,8 @@ __device__ __forceinline__ SubTile subtile_of(const P1Args &a, int s) {
     const int64_t t = blockIdx.x + (int64_t)(s / SUB) * gridDim.x;
     const int sub = s % SUB;
     SubTile st;
-    st.aH = a.aH0 + t / a.C;
-    st.c = t % a.C;
+    st.aH = a.aH0 + (t >> a.logC);
+    st.c = t & (a.C - 1);
     st.r1 = sub >> 1;
     st.b1 = sub & 1;
     return st;
@@ -905,6 +906,7 @@ struct VArgs {
     int64_t xa0, alo, ahi;
     int64_t A0, nA, ya0;
     int64_t nB;  // 2^(R-Q)
+    int logV, lognB;  // V and nB are powers of two: index math by shifts (64-bit div/mod is ~100 instructions)
     int vf1_batch;  // Q = 1: issue all row loads of 4 elements first (LRE_VF1=0 disables; A/B only)
     Final f;
 };
@@ -1003,10 +1005,10 @@ __global__ void __launch_bounds__(128, 4) vfold_kernel(const VArgs a) {
             for (int u = 0; u < U; ++u) {
                 const int64_t t = t0 + u * stride;
                 const int64_t V = opaque(a.V);
-                vv[u] = t % V;
-                const int64_t rest = t / V;
-                BB[u] = rest % a.nB;
-                AA[u] = a.A0 + rest / a.nB;
+                vv[u] = t & (V - 1);
+                const int64_t rest = t >> a.logV;
+                BB[u] = rest & (a.nB - 1);
+                AA[u] = a.A0 + (rest >> a.lognB);
                 const int64_t row0 = AA[u] * 3;
                 const Tin *p0 = in + ((row0 - a.xa0) * a.ncol + BB[u] * 2) * V + vv[u];
                 const int64_t rstride = a.ncol * V;
@@ -1038,10 +1040,10 @@ __global__ void __launch_bounds__(128, 4) vfold_kernel(const VArgs a) {
     } else {
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t V = opaque(a.V);
-        const int64_t v = t % V;
-        const int64_t rest = t / V;
-        const int64_t B = rest % a.nB;
-        const int64_t A = a.A0 + rest / a.nB;
+        const int64_t v = t & (V - 1);
+        const int64_t rest = t >> a.logV;
+        const int64_t B = rest & (a.nB - 1);
+        const int64_t A = a.A0 + (rest >> a.lognB);
         const int64_t row0 = A * R3;
         const Tin *p0 = in + ((row0 - a.xa0) * a.ncol + B * C2) * V + v;
         const int64_t rstride = a.ncol * V;
@@ -1090,10 +1092,10 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, 2) vfold3_kernel(const VArgs a
 
     auto task_coords = [&](int i, int64_t &A, int64_t &B, int64_t &v0) {
         const int64_t t = gw + (int64_t)i * nw;
-        v0 = (t % nvb) << 5;
-        const int64_t rest = t / nvb;
-        B = rest % a.nB;
-        A = a.A0 + rest / a.nB;
+        v0 = (t & (nvb - 1)) << 5;
+        const int64_t rest = t >> (a.logV - 5);
+        B = rest & (a.nB - 1);
+        A = a.A0 + (rest >> a.lognB);
     };
     auto issue = [&](int q) {
         if (q < nq) {
@@ -1529,6 +1531,7 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             a.naH = ps.nA;
             a.out_aH0 = fin ? 0 : ls.A0;
             a.C = ipow(2, R - ps.q);
+            a.logC = R - ps.q;
             a.f = f;
             a.f.kind = OUT_INTER;
             {
@@ -1557,6 +1560,8 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             a.nA = ps.nA;
             a.ya0 = fin ? 0 : ls.A0;
             a.nB = ipow(2, R - ps.q);
+            a.logV = 2 * done;
+            a.lognB = R - ps.q;
             static const int vf1 = [] {
                 const char *v = getenv("LRE_VF1");
                 return v && v[0] == '0' ? 0 : 1;

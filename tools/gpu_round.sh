@@ -19,13 +19,13 @@ for n in ${BENCH_NS:-12 14}; do
 done
 if [ -n "$NCU_N" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-    --log-file $O/launches_n$NCU_N.csv python bench.py --n $NCU_N --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > $O/ncu_bench.log 2>&1
+    --log-file $O/launches_n$NCU_N.csv python bench.py --n $NCU_N --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-step3 > $O/ncu_bench.log 2>&1
   echo "ncu rc=$?" >> $O/ncu_bench.log
 fi
 if [ -n "$NCU_FULL_N" ]; then
   for k in ${NCU_KERNELS:-tile_pass}; do
     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$k -s ${NCU_SKIP:-2} -c ${NCU_COUNT:-1} \
-      -o $O/full_n${NCU_FULL_N}_$k -f python bench.py --n $NCU_FULL_N --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > $O/ncu_full_$k.log 2>&1
+      -o $O/full_n${NCU_FULL_N}_$k -f python bench.py --n $NCU_FULL_N --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-step3 > $O/ncu_full_$k.log 2>&1
     echo "ncu full $k rc=$?" >> $O/ncu_full_$k.log
   done
 fi
