@@ -164,6 +164,22 @@ int lre_counts_from_outcomes(const uint16_t *outcomes, int n, int64_t shots, int
                              int count_dtype, lre_stream_t stream);
 
 /*
+ * Arbitrary (dense / mixed) states (reference
+ * simulate.py:114-151, :224-242).
+ * lre_dense_to_theta: rho (device, row-major 2^n x 2^n complex128, Hermitian)
+ *   -> theta (device, 4^n fp64, NATURAL order), the inverse of lre_assemble
+ *   (replaces simulate.dense_to_theta).  n <= 12.
+ * lre_generate_counts_theta: sampled counts of settings [w_begin, w_end) for
+ *   the state with Pauli coefficients theta (device, NATURAL): per setting
+ *   the outcome distribution is one WHT of theta on the setting's support
+ *   (replaces _theta_probability_block), then `shots` inverse-CDF draws from
+ *   a Philox4x32-10 stream keyed on (seed, setting, shot).  n <= 12.
+ */
+int lre_dense_to_theta(const double *rho, int n, double *theta, lre_stream_t stream);
+int lre_generate_counts_theta(const double *theta, int n, int64_t shots, uint64_t seed, int64_t w_begin,
+                              int64_t w_end, void *out, int count_dtype, lre_stream_t stream);
+
+/*
  * Error metrics on the device (reference metrics.py).
  *
  * lre_reduce: deterministic fp64 reduction of `count` doubles (device) into

@@ -40,6 +40,8 @@ _SIGNATURES = {
     "lre_generate_counts": (_i, [_i, _i, _i64, _i64, _u64, _i, _i64, _i64, _vp, _i, _vp]),
     "lre_generate_outcomes": (_i, [_i, _i, _i64, _i64, _u64, _i64, _i64, _vp, _vp]),
     "lre_counts_from_outcomes": (_i, [_vp, _i, _i64, _i64, _vp, _i, _vp]),
+    "lre_dense_to_theta": (_i, [_vp, _i, _vp, _vp]),
+    "lre_generate_counts_theta": (_i, [_vp, _i, _i64, _u64, _i64, _i64, _vp, _i, _vp]),
     "lre_reduce": (_i, [_i, _vp, _vp, _i64, ctypes.c_double, _vp, _vp]),
     "lre_truth_terms": (_i, [_vp, _i, _i, _i64, _vp, _vp]),
 }

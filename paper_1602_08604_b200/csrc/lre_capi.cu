@@ -32,6 +32,9 @@ int generate_outcomes_impl(int kind, int n, int64_t bits, int64_t shots, uint64_
                            int64_t w_end, uint16_t *out, cudaStream_t s);
 int counts_from_outcomes_impl(const uint16_t *outcomes, int n, int64_t shots, int64_t rows, void *counts, int dtype,
                               cudaStream_t s);
+int dense_to_theta_impl(const double *rho, int n, double *theta, cudaStream_t s);
+int generate_theta_impl(const double *theta, int n, int64_t shots, uint64_t seed, int64_t w_begin, int64_t w_end,
+                        void *out, int dtype, cudaStream_t s);
 int reduce_impl(int op, const double *a, const double *b, int64_t count, double scale, double *out, cudaStream_t s);
 int truth_terms_impl(const double *a, int n, int kind, int64_t bits, double *out, cudaStream_t s);
 }  // namespace lre
@@ -175,6 +178,21 @@ int lre_counts_from_outcomes(const uint16_t *outcomes, int n, int64_t shots, int
     if (shots > dtype_max(count_dtype)) return LRE_EOVERFLOW;
     return lre::counts_from_outcomes_impl(outcomes, n, shots, rows, counts, count_dtype,
                                           reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_dense_to_theta(const double *rho, int n, double *theta, lre_stream_t stream) {
+    if (!valid_n(n) || !rho || !theta) return LRE_EINVAL;
+    return lre::dense_to_theta_impl(rho, n, theta, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_generate_counts_theta(const double *theta, int n, int64_t shots, uint64_t seed, int64_t w_begin,
+                              int64_t w_end, void *out, int count_dtype, lre_stream_t stream) {
+    if (!valid_n(n) || !theta || !out || shots < 1 || w_begin < 0 || w_end < w_begin || w_end > pow3_i(n))
+        return LRE_EINVAL;
+    if (dtype_max(count_dtype) < 0) return LRE_EINVAL;
+    if (shots > dtype_max(count_dtype)) return LRE_EOVERFLOW;
+    return lre::generate_theta_impl(theta, n, shots, seed, w_begin, w_end, out, count_dtype,
+                                    reinterpret_cast<cudaStream_t>(stream));
 }
 
 int lre_reduce(int op, const double *a, const double *b, int64_t count, double scale, double *out,

@@ -17,6 +17,23 @@ __host__ __device__ constexpr int popc_c(int x) { return x == 0 ? 0 : (x & 1) + 
 // global launch counter (bench.py reports it as gpu_launches)
 void count_launch(int k = 1);
 
+// Philox4x32-10 (counter-based): the record generators key it on (seed) with
+// counters (shot, ..., setting), so records do not depend on launch shape.
+struct Philox {
+    __device__ __forceinline__ static uint4 gen(uint4 c, uint2 k) {
+#pragma unroll
+        for (int i = 0; i < 10; ++i) {
+            const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+            const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+            c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+            k.x += 0x9E3779B9u;
+            k.y += 0xBB67AE85u;
+        }
+        return c;
+    }
+};
+
+
 // ---------------------------------------------------------------------------
 // count loads: 8 consecutive elements of the counts / intermediate tensor,
 // streamed with the evict-first (".cs") policy so they do not displace the

@@ -94,8 +94,13 @@ def truth_terms(truth: StateDescriptor, a) -> tuple[float, float]:
 
 
 def hs_squared_distance_to_state(truth: StateDescriptor, a) -> float:
-    """Tr((a - rho_true)^2) = ||a||^2 - 2 Re Tr(a rho_true) + Tr(rho_true^2), without a dense truth."""
+    """Tr((a - rho_true)^2) = ||a||^2 - 2 Re Tr(a rho_true) + Tr(rho_true^2), without a dense truth
+    (dense states — ``random`` — are compared against their dense matrix)."""
     ta = _dev_tensor(a).to(_torch().complex128)
+    if truth.kind not in _lib.STATE_KINDS:
+        from .simulate import density_matrix
+
+        return hs_squared_distance(ta, _dev_tensor(density_matrix(truth), ta.device))
     cross, purity = truth_terms(truth, ta)
     return _reduce(_lib.REDUCE_SUM_SQ, _as_f64(ta)) - 2.0 * cross + purity
 
@@ -156,6 +161,10 @@ def fidelity_with_state(truth: StateDescriptor, sigma, eigenvalues=None) -> floa
     """F(rho_true, sigma) for a generator state: the spectrum for maxmixed,
     <psi|sigma|psi> for the pure states (the reference's 'auto' shortcuts)."""
     d = 1 << truth.n
+    if truth.kind not in _lib.STATE_KINDS:
+        from .simulate import density_matrix
+
+        return fidelity(density_matrix(truth), sigma)
     if truth.kind == "maxmixed":
         if eigenvalues is None:
             eigenvalues = _torch().linalg.eigvalsh(_dev_tensor(sigma).to(_torch().complex128))
@@ -190,21 +199,6 @@ def _pauli_theta_small(rho: np.ndarray, n: int) -> np.ndarray:
             m = np.kron(m, single[(a >> (2 * (n - 1 - q))) & 3])
         theta[a] = np.real(np.trace(rho @ m)) / np.sqrt(1 << n)
     return theta
-
-
-def _dense_truth_small(truth: StateDescriptor) -> np.ndarray:
-    """Dense rho_true of a generator state at n <= PREDICTOR_DENSE_MAX_QUBITS (host, tiny)."""
-    d = 1 << truth.n
-    if truth.kind == "maxmixed":
-        return np.eye(d, dtype=np.complex128) / d
-    psi = np.zeros(d, dtype=np.complex128)
-    if truth.kind == "ghz":
-        psi[0] = psi[d - 1] = 1.0 / np.sqrt(2.0)
-    elif truth.kind == "productz":
-        psi[truth.bits] = 1.0
-    else:
-        psi[[1 << k for k in range(truth.n)]] = 1.0 / np.sqrt(truth.n)
-    return np.outer(psi, psi.conj())
 
 
 def predicted_mse_dense(rho, n0: float) -> float:
@@ -264,7 +258,9 @@ def evaluate_errors(truth: StateDescriptor, rho_hat, mu_hat=None, n0: float | No
             predicted_hs = predicted_mse_max_mixed(n, n0)
             predicted_infid = predicted_infidelity_max_mixed(n, n0)
         elif n <= PREDICTOR_DENSE_MAX_QUBITS:
-            predicted_hs = predicted_mse_dense(_dense_truth_small(truth), n0)
+            from .simulate import density_matrix
+
+            predicted_hs = predicted_mse_dense(density_matrix(truth), n0)
     return ErrorReport(n=n, n0=n0, hs_squared_mu=hs_mu, hs_squared_rho=hs_rho, infidelity=infid,
                        predicted_hs=predicted_hs, predicted_infidelity=predicted_infid)
 

@@ -4,8 +4,10 @@ Mirrors the reference's state descriptors and record generators
 (simulate.py:26-83 StateDescriptor/parse_state, :224-242 sample_counts,
 :245-266 exact_record) with the counts written straight into HBM by
 ``lre_generate_counts``.  Supported states are the bond-dimension-2 family
-maxmixed / ghz / productz / w (W is new relative to the reference; the
-reference's dense ``random`` Ginibre states stay a test-side concern).
+maxmixed / ghz / productz / w (W is new relative to the reference), drawn
+directly from their closed forms, and any dense state — the reference's
+``random`` Ginibre states included — through its Pauli coefficients on the
+device (``lre_dense_to_theta`` + ``lre_generate_counts_theta``).
 """
 
 from __future__ import annotations
@@ -17,7 +19,9 @@ import numpy as np
 from . import _lib, pauli
 from .records import DeviceRecord, MeasurementRecord, compact_dtype
 
-KINDS = ("maxmixed", "ghz", "productz", "w")
+KINDS = ("maxmixed", "ghz", "productz", "w", "random")
+RANDOM_STATE_MAX_QUBITS = 8  # simulate.py:18 (dense Ginibre draw on the host)
+DENSE_MAX_QUBITS = 12  # simulate.py:19 (dense-state generator / lre_dense_to_theta)
 
 
 @dataclass(frozen=True)
@@ -35,10 +39,16 @@ class StateDescriptor:
             raise ValueError(f"unknown state kind {self.kind!r}")
         if self.kind == "productz" and not 0 <= self.bits < (1 << n):
             raise ValueError(f"productz bits {self.bits} out of range for n={n}")
+        if self.kind == "random" and n > RANDOM_STATE_MAX_QUBITS:
+            raise ValueError(
+                f"random states need dense {2**n}x{2**n} storage; capped at n={RANDOM_STATE_MAX_QUBITS}"
+            )
 
     def label(self) -> str:
         if self.kind == "productz":
             return f"productz:{self.bits:0{self.n}b}"
+        if self.kind == "random":
+            return f"random:{self.state_seed}"
         return self.kind
 
     @property
@@ -65,7 +75,101 @@ def parse_state(text: str, n: int) -> StateDescriptor:
             return StateDescriptor("productz", n, bits=int(arg))
         except ValueError:
             raise ValueError(f"bad productz argument {arg!r}") from None
+    if name == "random":
+        try:
+            return StateDescriptor("random", n, state_seed=int(arg))
+        except ValueError:
+            raise ValueError(f"bad random-state seed {arg!r}") from None
     raise ValueError(f"unknown state {text!r}")
+
+
+def density_matrix(state: StateDescriptor) -> np.ndarray:
+    """Dense rho of a state on the host (simulate.py:86-111); n <= DENSE_MAX_QUBITS."""
+    n = state.n
+    if n > DENSE_MAX_QUBITS:
+        raise ValueError(f"dense matrix at n={n} exceeds the {DENSE_MAX_QUBITS}-qubit cap")
+    d = 1 << n
+    if state.kind == "maxmixed":
+        return np.eye(d, dtype=np.complex128) / d
+    if state.kind == "random":
+        # Ginibre ensemble G G^dag / Tr, G with iid standard complex normal
+        # entries from numpy's default_rng(state_seed) (simulate.py:105-111)
+        rng = np.random.default_rng(state.state_seed)
+        g = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+        rho = g @ g.conj().T
+        return rho / np.trace(rho).real
+    psi = np.zeros(d, dtype=np.complex128)
+    if state.kind == "ghz":
+        psi[0] = psi[d - 1] = 1.0 / np.sqrt(2.0)
+    elif state.kind == "productz":
+        psi[state.bits] = 1.0
+    else:  # w
+        psi[[1 << k for k in range(n)]] = 1.0 / np.sqrt(n)
+    return np.outer(psi, psi.conj())
+
+
+def dense_to_theta(rho, device=None, stream=None):
+    """Pauli coefficients (NATURAL, fp64, on the device) of a dense Hermitian
+    2^n x 2^n matrix: lre_dense_to_theta, the inverse of step (ii)
+    (replaces simulate.py:114-138)."""
+    import torch
+
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    r = rho if isinstance(rho, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(rho, dtype=np.complex128))
+    r = r.to(device=device, dtype=torch.complex128).contiguous()
+    d = int(r.shape[0])
+    n = d.bit_length() - 1
+    if r.dim() != 2 or int(r.shape[1]) != d or (1 << n) != d:
+        raise ValueError(f"expected a square 2**n x 2**n matrix, got {tuple(r.shape)}")
+    if n > DENSE_MAX_QUBITS:
+        raise ValueError(f"dense matrix at n={n} exceeds the {DENSE_MAX_QUBITS}-qubit cap")
+    theta = torch.empty(4**n, dtype=torch.float64, device=device)
+    stream = stream if stream is not None else torch.cuda.current_stream(device)
+    _lib.call("lre_dense_to_theta", r.data_ptr(), n, theta.data_ptr(), stream.cuda_stream)
+    return theta
+
+
+_THETA_CACHE: dict = {}
+
+
+def state_theta(state: StateDescriptor, device=None):
+    """Device theta of a state through its dense matrix (cached per state and device)."""
+    import torch
+
+    device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    key = (state, str(device))
+    if key not in _THETA_CACHE:
+        _THETA_CACHE.clear()  # one state at a time: theta is 8 * 4^n bytes
+        _THETA_CACHE[key] = dense_to_theta(density_matrix(state), device=device)
+    return _THETA_CACHE[key]
+
+
+def generate_counts_from_theta(theta, n: int, shots: int, seed: int = 0, w_begin: int = 0, w_end: int | None = None,
+                               dtype=None, out=None, stream=None):
+    """Counts rows [w_begin, w_end) of the state with Pauli coefficients theta
+    (device, NATURAL), drawn on the device (lre_generate_counts_theta)."""
+    import torch
+
+    from .records import lre_dtype_of
+
+    w_end = 3**n if w_end is None else int(w_end)
+    dtype = compact_dtype(shots) if dtype is None else dtype
+    if out is None:
+        out = torch.empty((w_end - w_begin, 1 << n), dtype=_torch_dtype(dtype), device=theta.device)
+    stream = stream if stream is not None else torch.cuda.current_stream(theta.device)
+    _lib.call("lre_generate_counts_theta", theta.data_ptr(), n, int(shots), int(seed) & 0xFFFFFFFFFFFFFFFF,
+              int(w_begin), int(w_end), out.data_ptr(), lre_dtype_of(out.dtype), stream.cuda_stream)
+    return out
+
+
+def sample_counts_from_density(rho, shots: int, seed: int, dtype=None, device=None) -> DeviceRecord:
+    """Sampled record of an arbitrary dense state (n <= 12), drawn on the device."""
+    if shots < 1:
+        raise ValueError(f"shots must be >= 1, got {shots}")
+    theta = dense_to_theta(rho, device=device)
+    n = (int(theta.shape[0]).bit_length() - 1) // 2
+    counts = generate_counts_from_theta(theta, n, shots, seed, dtype=dtype)
+    return DeviceRecord(n=n, shots=shots, counts=counts, seed=seed, state="dense")
 
 
 def _torch_dtype(np_dtype):
@@ -90,6 +194,13 @@ def generate_device_counts(state: StateDescriptor, shots: int, seed: int = 0, ex
     stream = stream if stream is not None else torch.cuda.current_stream(device)
     from .records import lre_dtype_of
 
+    if state.kind == "random":
+        if exact:
+            raise ValueError(
+                f"state {state.label()} has non-dyadic probabilities; an exact integer record does not exist"
+            )
+        return generate_counts_from_theta(state_theta(state, device), n, shots, seed, w_begin, w_end, out=out,
+                                          stream=stream)
     try:
         _lib.call("lre_generate_counts", _lib.STATE_KINDS[state.kind], n, int(state.bits), int(shots),
                   int(seed) & 0xFFFFFFFFFFFFFFFF, 1 if exact else 0, int(w_begin), int(w_end), out.data_ptr(),
@@ -129,6 +240,8 @@ def generate_device_outcomes(state: StateDescriptor, shots: int, seed: int = 0, 
     import torch
 
     n = state.n
+    if state.kind not in _lib.STATE_KINDS:
+        raise ValueError(f"outcome lists are generated for {sorted(_lib.STATE_KINDS)} states, not {state.label()}")
     w_end = 3**n if w_end is None else int(w_end)
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     if out is None:

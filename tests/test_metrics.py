@@ -102,10 +102,10 @@ class TestDeviceMetrics:
             assert close(M.truth_terms(st, a)[0], float(np.trace(a @ truth).real), 1e-12)
 
     def test_predicted_mse_state_any_n(self, torch_cuda):
-        from paper_1602_08604_b200.metrics import _dense_truth_small
+        from paper_1602_08604_b200.simulate import density_matrix
 
         st = lre.StateDescriptor("ghz", 4)
-        assert close(M.predicted_mse_state(st, 11.0), M.predicted_mse_dense(_dense_truth_small(st), 11.0), 1e-12)
+        assert close(M.predicted_mse_state(st, 11.0), M.predicted_mse_dense(density_matrix(st), 11.0), 1e-12)
         n = 10  # productz: sum_{w,s} p^2 = 2^n in closed form
         want = (5 / 9) ** n * (3**n - 2**n) / (7.0 * 2**n)
         assert close(M.predicted_mse_state(lre.StateDescriptor("productz", n, bits=77), 7.0), want, 1e-12)
