@@ -11,7 +11,9 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "liblre_b200.so")
+# LRE_LIB_PATH: an alternative build of the same library (A/B experiments of
+# compile-time variants, tools/debug/); the default is the in-tree build.
+LIB_PATH = os.environ.get("LRE_LIB_PATH") or os.path.join(_HERE, "_lib", "liblre_b200.so")
 
 LRE_OK, LRE_EINVAL, LRE_ECUDA, LRE_ENOMEM, LRE_EUNSUPPORTED, LRE_EOVERFLOW = range(6)
 U8, U16, I32, I64 = 1, 2, 3, 4

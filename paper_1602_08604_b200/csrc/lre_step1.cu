@@ -1006,7 +1006,13 @@ __device__ __forceinline__ void vblock(Ld ld, Sink sink) {
 }
 
 template <int Q, typename Tin, typename Ta, bool FINAL>
-__global__ void __launch_bounds__(128, 4) vfold_kernel(const VArgs a) {
+#ifndef VF1_MINB
+#define VF1_MINB 8
+#endif
+#ifndef VF1_U
+#define VF1_U 2
+#endif
+__global__ void __launch_bounds__(128, Q == 1 ? VF1_MINB : 4) vfold_kernel(const VArgs a) {
     constexpr int R3 = Q == 1 ? 3 : Q == 2 ? 9 : 27;
     constexpr int C2 = 1 << Q;
     constexpr int NOUT = 1 << (2 * Q);
@@ -1017,7 +1023,7 @@ __global__ void __launch_bounds__(128, 4) vfold_kernel(const VArgs a) {
         // One qubit: each thread issues the six row loads of VF1_U elements
         // before any arithmetic (the r1-streamed vblock keeps only two loads
         // in flight, which held the final n = 14 pass at 2.4 TB/s).
-        constexpr int U = 4;
+        constexpr int U = VF1_U;
         const int64_t stride = (int64_t)gridDim.x * blockDim.x;
         for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < total; t0 += U * stride) {
             Ta x[U][6];
