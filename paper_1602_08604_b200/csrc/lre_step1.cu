@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
                             [&](int D6, const int32_t(&v)[16]) { stage_record<SMALL>(rec, D6, v); });
                 }
             }
-            asm volatile("bar.sync 0;" ::: "memory");
+            asm volatile("barrier.sync 0;" ::: "memory");  // non-.aligned: L1 and L2 warps reach it from different code
         }
     } else {
         for (int s = 0; s <= S; ++s) {
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
                 l2_subtile<Q, SMALL>(a, subtile_of<Q>(a, s - 1),
                                      reinterpret_cast<const T *>(smem + ((s - 1) & 1) * ST::BYTES),
                                      tid - 32 * P1_L1_WARPS, tmp, oi);
-            asm volatile("bar.sync 0;" ::: "memory");
+            asm volatile("barrier.sync 0;" ::: "memory");  // non-.aligned: L1 and L2 warps reach it from different code
         }
     }
 }

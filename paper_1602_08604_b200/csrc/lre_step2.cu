@@ -203,6 +203,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) assemble_pair
     const int64_t ncl = gridDim.x / 2;
     double *dst0 = rank == 0 ? sbuf : cluster.map_shared_rank(sbuf, 0);  // mask m0's buffer
     double *dst1 = rank == 1 ? sbuf : cluster.map_shared_rank(sbuf, 1);  // mask m0 + 1's buffer
+    cluster.sync();  // the partner CTA has started before its shared memory is written
     for (int64_t grp = blockIdx.x / 2; grp < a.groups; grp += ncl) {
         const int64_t mloc0 = grp * 2;
         const uint32_t m0 = (uint32_t)(a.m_begin + mloc0);

@@ -1,0 +1,45 @@
+"""Small instances of every product kernel, for compute-sanitizer
+(memcheck / racecheck / synccheck):
+    compute-sanitizer --tool memcheck python tools/debug/sanitize_smoke.py
+Set LRE_ASM_BUDGET_KB=8 to route n = 10 assembly through the 2-CTA cluster
+kernel (used at n = 14 by default)."""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+import paper_1602_08604_b200 as lre  # noqa: E402
+from paper_1602_08604_b200 import metrics as M  # noqa: E402
+from paper_1602_08604_b200 import simulate as S  # noqa: E402
+
+
+def main():
+    lre.reconstruct(lre.sample_counts(lre.StateDescriptor("w", 7), 70000, seed=1), project=False)
+    for n, shots, kind in [(8, 1000, "ghz"), (10, 500, "w")]:
+        st = lre.StateDescriptor(kind, n)
+        rec = lre.sample_counts(st, shots, seed=1)
+        res = lre.reconstruct(rec, project=False, as_tensor=True)
+        plan = lre.LREPlan(n, shots)
+        s = torch.cuda.current_stream()
+        q = 3**min(n, 7)
+        for lo in range(0, 3**n, q):
+            plan.stage(rec.counts[lo:lo + q], rec.lre_dtype, lo, min(3**n, lo + q), s)
+        plan.finish(s)
+        plan.step2(s)
+        assert torch.equal(plan.theta, res.theta)
+    big = lre.sample_counts(lre.StateDescriptor("ghz", 5), 3_000_000_000, seed=2, dtype=np.int64)
+    lre.reconstruct(big, project=False)
+    o = lre.sample_outcomes(lre.StateDescriptor("ghz", 9), 300, seed=3)
+    lre.reconstruct(o, project=False)
+    rho = S.density_matrix(lre.StateDescriptor("random", 6, state_seed=4))
+    rec = S.sample_counts_from_density(rho, 200, seed=5)
+    res = lre.reconstruct(rec, project=True, as_tensor=True)
+    M.evaluate_errors(lre.StateDescriptor("ghz", 6), res.rho, res.mu, n0=3.0)
+    M.hs_squared_distance(res.mu, torch.from_numpy(rho).cuda())
+    torch.cuda.synchronize()
+    print("sanitize smoke ok")
+
+
+if __name__ == "__main__":
+    main()
