@@ -220,7 +220,7 @@ def e2e_host(plan, slabs, n, mu_host, chunk_rows, steps, warmup, torch, lre_dtyp
                     bufs[b][: hi - lo].copy_(slab[lo - s_lo:hi - s_lo], non_blocking=True)
                     ev_copy[b].record(copy)
                 comp.wait_event(ev_copy[b])
-                plan.stage(bufs[b], lre_dtype, lo, hi, comp)
+                plan.stage(bufs[b][: hi - lo], lre_dtype, lo, hi, comp, validate=True)
                 ev_used[b].record(comp)
                 k += 1
         plan.finish(comp)
@@ -239,6 +239,7 @@ def e2e_host(plan, slabs, n, mu_host, chunk_rows, steps, warmup, torch, lre_dtyp
     e1.record(comp)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    plan.verify()  # the chunks were validated on the device inside the timed region; raise if any row was bad
     del bufs
     return e0.elapsed_time(e1) / 1e3 / steps, wall / steps
 
@@ -280,7 +281,7 @@ def e2e_outcomes(plan, st, shots, seed, n, mu_host, chunk_rows, steps, torch):
                 bufs[b][: hi - lo].copy_(h, non_blocking=True)
                 ev_copy[b].record(copy)
             comp.wait_event(ev_copy[b])
-            plan.stage_outcomes(bufs[b][: hi - lo], lo, hi, comp)
+            plan.stage_outcomes(bufs[b][: hi - lo], lo, hi, comp, validate=True)
             ev_used[b].record(comp)
         plan.finish(comp)
         plan.step2(comp)
@@ -297,6 +298,7 @@ def e2e_outcomes(plan, st, shots, seed, n, mu_host, chunk_rows, steps, torch):
     e1.record(comp)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
+    plan.verify()
     h2d = sum(h.numel() * 2 for _, _, h in host)
     del bufs, host
     plan._dense = None
@@ -404,7 +406,8 @@ def run_b200(args):
                        "d2h_bytes_per_step": int(mu_host.numel() * mu_host.element_size()),
                        "wall_s_per_step": wall_e2e, "host_memory": "pinned" if pinned else "pageable",
                        "steps": ksteps,
-                       "api": "LREPlan.stage/finish/step2 (lre_step1_stage/finish, lre_assemble) from host counts"}
+                       "api": "LREPlan.stage(validate=True)/finish/step2 (lre_validate_counts + lre_step1_stage, "
+                              "lre_step1_finish, lre_assemble) from host counts"}
                 del slabs, mu_host
             except Exception as exc:  # keep the device-side line even if the host side fails
                 e2e = {"value": None, "unit": "s", "error": f"{type(exc).__name__}: {str(exc)[:200]}"}

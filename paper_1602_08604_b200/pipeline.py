@@ -160,17 +160,43 @@ class LREPlan:
         self.theta = torch.empty(4**self.n, dtype=torch.float64, device=self.device)
         self.mu = self.ws[:mu_bytes].view(torch.complex128).view(d, d) if with_mu else None
         self.passes = int(L.lre_step1_num_passes(self.n, self.shots))
+        self._checks = []
 
     def step1(self, counts, count_dtype: int, stream) -> None:
         _lib.call("lre_step1", counts.data_ptr(), count_dtype, self.n, self.shots, 0, 3**self.n,
                   self.ws.data_ptr(), self.ws_bytes, self.theta.data_ptr(), _lib.OUT_THETA_F64,
                   _lib.NATURAL, stream.cuda_stream)
 
-    def stage(self, chunk, count_dtype: int, w_begin: int, w_end: int, stream) -> None:
+    def stage(self, chunk, count_dtype: int, w_begin: int, w_end: int, stream, validate: bool = False) -> None:
+        """Fold setting chunk [w_begin, w_end) into the first pass (lre_step1_stage).
+
+        validate=True also checks the chunk's rows on the device
+        (lre_validate_counts, records.py:34-56) on the same stream; the result
+        is read by verify(), which raises the reference's message for the
+        first bad setting — the streaming counterpart of validating a record
+        before the reconstruction."""
+        if validate:
+            torch = _torch()
+            res = torch.empty(3, dtype=torch.int64, device=self.device)
+            _lib.call("lre_validate_counts", chunk.data_ptr(), count_dtype, self.n, int(w_end) - int(w_begin),
+                      self.shots, res.data_ptr(), stream.cuda_stream)
+            self._checks.append((int(w_begin), res))
         _lib.call("lre_step1_stage", chunk.data_ptr(), count_dtype, self.n, self.shots, int(w_begin), int(w_end),
                   self.ws.data_ptr(), self.ws_bytes, stream.cuda_stream)
 
-    def stage_outcomes(self, outcomes, w_begin: int, w_end: int, stream) -> None:
+    def verify(self) -> None:
+        """Raise for the first invalid row among the chunks staged with validate=True (synchronises)."""
+        checks, self._checks = self._checks, []
+        for w0, res in checks:
+            first_bad, bad_sum, min_value = (int(x) for x in res.cpu().tolist())
+            if min_value < 0:
+                raise ValueError("counts must be non-negative")
+            if first_bad != (1 << 63) - 1:
+                w = w0 + first_bad
+                raise ValueError(f"setting {pauli.setting_label(w, self.n)} (index {w}) sums to {bad_sum}, "
+                                 f"expected {self.shots}")
+
+    def stage_outcomes(self, outcomes, w_begin: int, w_end: int, stream, validate: bool = False) -> None:
         """Streaming ingestion of an outcome-list chunk: histogram on the device, then stage."""
         torch = _torch()
         rows = int(outcomes.shape[0])
@@ -180,7 +206,7 @@ class LREPlan:
             self._dense = buf = torch.empty((rows, 1 << self.n), dtype=dt, device=self.device)
         dense = buf[:rows]
         counts_from_outcomes(outcomes, self.n, self.shots, out=dense, stream=stream)
-        self.stage(dense, lre_dtype_of(dense.dtype), w_begin, w_end, stream)
+        self.stage(dense, lre_dtype_of(dense.dtype), w_begin, w_end, stream, validate=validate)
 
     def finish(self, stream) -> None:
         _lib.call("lre_step1_finish", self.ws.data_ptr(), self.ws_bytes, self.n, self.shots,

@@ -273,7 +273,6 @@ def reconstruct_file(path_or_file, *, device=None, project: bool = False, chunk_
     dbuf = [torch.empty((chunk, rf.data.shape[1]), dtype=tdt, device=dev) for _ in range(2)]
     done = [torch.cuda.Event() for _ in range(2)]
     used = [torch.cuda.Event() for _ in range(2)]
-    checks = []
     view_dt = {np.dtype("<u1"): torch.uint8, np.dtype("<u2"): torch.uint16, np.dtype("<i4"): torch.int32,
                np.dtype("<i8"): torch.int64}[rf.data.dtype]
     t0 = time.perf_counter()
@@ -289,14 +288,9 @@ def reconstruct_file(path_or_file, *, device=None, project: bool = False, chunk_
         comp.wait_event(done[b])
         block = dbuf[b][: hi - lo].view(view_dt)
         if rf.layout == LAYOUT_OUTCOMES:
-            plan.stage_outcomes(block, lo, hi, comp)
-            block = plan._dense[: hi - lo]
+            plan.stage_outcomes(block, lo, hi, comp, validate=True)
         else:
-            plan.stage(block, lre_dtype_of(view_dt), lo, hi, comp)
-        res = torch.empty(3, dtype=torch.int64, device=dev)
-        _lib.call("lre_validate_counts", block.data_ptr(), lre_dtype_of(block.dtype), n, hi - lo, shots,
-                  res.data_ptr(), comp.cuda_stream)
-        checks.append((lo, res))
+            plan.stage(block, lre_dtype_of(view_dt), lo, hi, comp, validate=True)
         used[b].record(comp)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     ev[0].record(comp)
@@ -305,13 +299,7 @@ def reconstruct_file(path_or_file, *, device=None, project: bool = False, chunk_
     ev[1].record(comp)
     plan.step2(comp)
     ev[2].record(comp)
-    for lo, res in checks:
-        first_bad, bad_sum, min_value = (int(x) for x in res.cpu().tolist())
-        if min_value < 0:
-            raise ValueError("counts must be non-negative")
-        if first_bad != (1 << 63) - 1:
-            raise ValueError(f"setting {pauli.setting_label(lo + first_bad, n)} (index {lo + first_bad}) sums to "
-                             f"{bad_sum}, expected {shots}")
+    plan.verify()
     rho, evals = step_three_project(plan.mu) if project else (plan.mu, None)
     ev[3].record(comp)
     ev[3].synchronize()
