@@ -81,6 +81,13 @@ class ClockSampler:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if not self.lines:  # region shorter than nvidia-smi's start-up: one query at its end
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=20)
+                self.lines.extend(l.strip() for l in out.stdout.splitlines() if l.strip())
+            except Exception:
+                pass
 
     def summary(self):
         sm, mx, reasons = [], None, set()
