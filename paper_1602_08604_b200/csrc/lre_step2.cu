@@ -277,10 +277,15 @@ int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64
         cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
     }
     const int Dp = (int)(d + (d >> 4) + 1);
-    static const size_t smem_budget = [] {
-        const char *v = getenv("LRE_ASM_BUDGET_KB");  // A/B experiments only
-        return (size_t)(v ? atoi(v) : 150) * 1024;
+    // shared-memory budget per CTA (masks per CTA = largest power of two that
+    // fits): measured best 40 KB at n <= 11 (several CTAs per SM), 75 KB at
+    // n = 12, 150 KB at n = 13 (profiles/README.md); LRE_ASM_BUDGET_KB
+    // overrides it for A/B runs
+    static const int budget_env = [] {
+        const char *v = getenv("LRE_ASM_BUDGET_KB");
+        return v ? atoi(v) : 0;
     }();
+    const size_t smem_budget = (size_t)(budget_env > 0 ? budget_env : n <= 11 ? 40 : n == 12 ? 75 : 150) * 1024;
     int logb = 0;
     while (logb < 3 && ((int64_t)2 << logb) <= S && (size_t)(2 << logb) * Dp * sizeof(double) <= smem_budget) ++logb;
     AsmArgs a;
