@@ -1100,12 +1100,21 @@ __global__ void __launch_bounds__(128, Q == 1 ? VF1_MINB : 4) vfold_kernel(const
 // and writes whole 128-byte lines.  (Q = 3 cuts the n = 14 step-(i) traffic
 // from 223 GB (7+2+2+2+1) to 210 GB (7+3+3+1); the register-only vfold
 // would need 216 runtime-strided 64-bit addresses per thread.)
-constexpr int VF3_WARPS = 4;
+#ifndef VF3_W
+#define VF3_W 8
+#endif
+#ifndef VF3_S
+#define VF3_S 3
+#endif
+#ifndef VF3_MINB
+#define VF3_MINB 1
+#endif
+constexpr int VF3_WARPS = VF3_W;
 constexpr int VF3_GROUP_CHUNKS = 72 * 8;  // 16-byte chunks per r1 group (72 lines x 128 B)
-constexpr int VF3_SLOTS = 3;
+constexpr int VF3_SLOTS = VF3_S;
 
 template <bool FINAL>
-__global__ void __launch_bounds__(32 * VF3_WARPS, 2) vfold3_kernel(const VArgs a) {
+__global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const VArgs a) {
     extern __shared__ __align__(16) int4 vsm4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int4 *ring = vsm4 + warp * VF3_SLOTS * VF3_GROUP_CHUNKS;
@@ -1145,12 +1154,11 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, 2) vfold3_kernel(const VArgs a
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
 
-    issue(0);
-    issue(1);
-    issue(2);
+#pragma unroll
+    for (int k = 0; k < VF3_SLOTS; ++k) issue(k);
     int32_t Iacc[16];
     for (int q = 0; q < nq; ++q) {
-        asm volatile("cp.async.wait_group 2;" ::: "memory");
+        asm volatile("cp.async.wait_group %0;" ::"n"(VF3_SLOTS - 1) : "memory");
         __syncwarp();
         const int r1 = q % 3;
         int64_t A, B, v0;
@@ -1187,7 +1195,7 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, 2) vfold3_kernel(const VArgs a
                                w[b1][0 * 4 + d3], w[b1][1 * 4 + d3], w[b1][2 * 4 + d3], w[b1][3 * 4 + d3]);
         }
         __syncwarp();
-        issue(q + 3);  // this slot's data is in registers now
+        issue(q + VF3_SLOTS);  // this slot's data is in registers now
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
             Iacc[k] += w[0][k] + w[1][k];
@@ -1450,7 +1458,7 @@ static cudaError_t launch_vfold3(const VArgs &a, cudaStream_t s) {
     const size_t smem = (size_t)VF3_WARPS * VF3_SLOTS * VF3_GROUP_CHUNKS * sizeof(int4);
     const int64_t tasks = a.nA * a.nB * (a.V >> 5);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + VF3_WARPS - 1) / VF3_WARPS,
-                                                                (int64_t)g_num_sms * 2));
+                                                                (int64_t)g_num_sms * VF3_MINB));
     cudaError_t e;
     if (a.f.kind == OUT_INTER) {
         e = cudaFuncSetAttribute(vfold3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
