@@ -348,6 +348,14 @@ __device__ __forceinline__ int staged_col_to_dlo(int col) {
     return D4 * 16 + D5 * 4 + D6;
 }
 
+// The per-sub-tile CTA barrier of the tile pass.  The L1 and L2 warps run
+// separate loops and so reach it from different code; PTX requires the
+// non-.aligned form there (compute-sanitizer synccheck flags bar.sync).
+// Measured A/B at n = 14 (profiles/README.md): the inline .aligned form is
+// ~1.1 % faster but undefined behaviour; a shared non-inlined .aligned
+// barrier costs the same as this one.
+__device__ __forceinline__ void p1_step_barrier() { asm volatile("barrier.sync 0;" ::: "memory"); }
+
 // Sub-tile s of this CTA -> tile, top setting digit r1, top outcome bit b1
 struct SubTile {
     int64_t aH, c;
@@ -521,7 +529,7 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
                             [&](int D6, const int32_t(&v)[16]) { stage_record<SMALL>(rec, D6, v); });
                 }
             }
-            asm volatile("barrier.sync 0;" ::: "memory");  // non-.aligned: L1 and L2 warps reach it from different code
+            p1_step_barrier();
         }
     } else {
         for (int s = 0; s <= S; ++s) {
@@ -529,7 +537,7 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
                 l2_subtile<Q, SMALL>(a, subtile_of<Q>(a, s - 1),
                                      reinterpret_cast<const T *>(smem + ((s - 1) & 1) * ST::BYTES),
                                      tid - 32 * P1_L1_WARPS, tmp, oi);
-            asm volatile("barrier.sync 0;" ::: "memory");  // non-.aligned: L1 and L2 warps reach it from different code
+            p1_step_barrier();
         }
     }
 }
