@@ -203,6 +203,42 @@ def host_record(counts, chunk_rows, torch):
     raise MemoryError("could not stage the record in host memory")
 
 
+class MuPipe:
+    """Step (ii) into one of two device buffers and its D2H on a side stream:
+    step k's mu copy-out overlaps step k+1's H2D (PCIe is full duplex).
+    Every step's result still reaches pinned host memory inside the timed
+    region (drain() before the closing event)."""
+
+    def __init__(self, plan, mu_host, torch):
+        from paper_1602_08604_b200 import _lib
+
+        self.lib, self.plan, self.torch = _lib, plan, torch
+        d = 1 << plan.n
+        self.dev = [torch.empty((d, d), dtype=torch.complex128, device=plan.device) for _ in range(2)]
+        self.host = [mu_host, torch.empty_like(mu_host, pin_memory=True)]
+        self.d2h = torch.cuda.Stream(plan.device)
+        self.done = [torch.cuda.Event() for _ in range(2)]
+        self.k = 0
+
+    def assemble_and_copy(self, comp):
+        b = self.k % 2
+        comp.wait_event(self.done[b])  # the previous copy-out of this buffer has finished
+        d = 1 << self.plan.n
+        self.lib.call("lre_assemble", self.plan.theta.data_ptr(), self.lib.NATURAL, self.plan.n, 0, d,
+                      self.dev[b].data_ptr(), comp.cuda_stream)
+        ready = self.torch.cuda.Event()
+        ready.record(comp)
+        self.d2h.wait_event(ready)
+        with self.torch.cuda.stream(self.d2h):
+            self.host[b].copy_(self.dev[b], non_blocking=True)
+            self.done[b].record(self.d2h)
+        self.k += 1
+
+    def drain(self, comp):
+        for e in self.done:
+            comp.wait_event(e)
+
+
 def e2e_host(plan, slabs, n, mu_host, chunk_rows, steps, warmup, torch, lre_dtype):
     """Public streaming API from HOST counts: H2D chunks (copy stream)
     overlapped with the first pass (lre_step1_stage), then the remaining
@@ -215,6 +251,7 @@ def e2e_host(plan, slabs, n, mu_host, chunk_rows, steps, warmup, torch, lre_dtyp
     bufs = [torch.empty((chunk_rows, width), dtype=slabs[0][2].dtype, device=dev) for _ in range(2)]
     ev_copy = [torch.cuda.Event() for _ in range(2)]
     ev_used = [torch.cuda.Event() for _ in range(2)]
+    pipe = MuPipe(plan, mu_host, torch)
 
     def one():
         k = 0
@@ -231,11 +268,11 @@ def e2e_host(plan, slabs, n, mu_host, chunk_rows, steps, warmup, torch, lre_dtyp
                 ev_used[b].record(comp)
                 k += 1
         plan.finish(comp)
-        plan.step2(comp)
-        mu_host.copy_(plan.mu, non_blocking=True)
+        pipe.assemble_and_copy(comp)
 
     for _ in range(warmup):
         one()
+    pipe.drain(comp)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -243,6 +280,7 @@ def e2e_host(plan, slabs, n, mu_host, chunk_rows, steps, warmup, torch, lre_dtyp
     e0.record(comp)
     for _ in range(steps):
         one()
+    pipe.drain(comp)
     e1.record(comp)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
@@ -279,6 +317,7 @@ def e2e_outcomes(plan, st, shots, seed, n, mu_host, chunk_rows, steps, torch):
     bufs = [torch.empty((chunk_rows, shots), dtype=torch.uint16, device=dev) for _ in range(2)]
     ev_copy = [torch.cuda.Event() for _ in range(2)]
     ev_used = [torch.cuda.Event() for _ in range(2)]
+    pipe = MuPipe(plan, mu_host, torch)
 
     def one():
         for k, (lo, hi, h) in enumerate(host):
@@ -291,10 +330,10 @@ def e2e_outcomes(plan, st, shots, seed, n, mu_host, chunk_rows, steps, torch):
             plan.stage_outcomes(bufs[b][: hi - lo], lo, hi, comp, validate=True)
             ev_used[b].record(comp)
         plan.finish(comp)
-        plan.step2(comp)
-        mu_host.copy_(plan.mu, non_blocking=True)
+        pipe.assemble_and_copy(comp)
 
     one()
+    pipe.drain(comp)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -302,6 +341,7 @@ def e2e_outcomes(plan, st, shots, seed, n, mu_host, chunk_rows, steps, torch):
     e0.record(comp)
     for _ in range(steps):
         one()
+    pipe.drain(comp)
     e1.record(comp)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
@@ -381,6 +421,9 @@ def run_b200(args):
     t_pass1 = e[0].elapsed_time(e[1]) / 1e3 / k
     t_rest1 = e[1].elapsed_time(e[2]) / 1e3 / k
     t_asm = e[2].elapsed_time(e[3]) / 1e3 / k
+    # the repeated finish() above re-reads ping-ponged intermediates: restore a
+    # valid theta / mu (used by step iii when the e2e runs are skipped)
+    plan.run(counts, lre_dtype, s)
     pass1_bytes = c * 6.0**n  # algorithmic: every count read once (the Y1 write is not counted)
     q1 = min(n, 7)
     tma = counts.dtype == torch.uint16 and shots <= 1213 and n >= 6 and os.environ.get("LRE_P1") == "tma"
@@ -413,8 +456,11 @@ def run_b200(args):
                        "d2h_bytes_per_step": int(mu_host.numel() * mu_host.element_size()),
                        "wall_s_per_step": wall_e2e, "host_memory": "pinned" if pinned else "pageable",
                        "steps": ksteps,
-                       "api": "LREPlan.stage(validate=True)/finish/step2 (lre_validate_counts + lre_step1_stage, "
-                              "lre_step1_finish, lre_assemble) from host counts"}
+                       "api": "LREPlan.stage(validate=True)/finish + lre_assemble (lre_validate_counts + "
+                              "lre_step1_stage, lre_step1_finish, lre_assemble) from host counts",
+                       "pipelining": "mu of step k is copied out on a side stream while step k+1's counts go in "
+                                     "(double-buffered device mu); every step's H2D and D2H complete inside the "
+                                     "timed region"}
                 del slabs, mu_host
             except Exception as exc:  # keep the device-side line even if the host side fails
                 e2e = {"value": None, "unit": "s", "error": f"{type(exc).__name__}: {str(exc)[:200]}"}
@@ -448,6 +494,7 @@ def run_b200(args):
         rec = counts = None  # free the record (157 GB at n = 14) for the eigensolver's workspace
         torch.cuda.empty_cache()
         try:
+            plan.step2(s)  # mu of the last reconstruction (the e2e runs assemble into their own buffers)
             warm = torch.eye(64, dtype=torch.complex128, device=dev) / 64  # cuSOLVER handle + module load
             lre.step_three_project(warm)
             torch.cuda.synchronize()
