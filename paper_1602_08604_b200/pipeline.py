@@ -121,6 +121,8 @@ def counts_from_outcomes(outcomes, n: int, shots: int, out=None, stream=None):
     rows = int(outcomes.shape[0])
     if out is None:
         out = torch.empty((rows, 1 << n), dtype=_torch_count_dtype(compact_dtype(shots)), device=outcomes.device)
+    if rows == 0:
+        return out
     stream = stream if stream is not None else torch.cuda.current_stream(outcomes.device)
     _lib.call("lre_counts_from_outcomes", outcomes.data_ptr(), n, int(shots), rows, out.data_ptr(),
               lre_dtype_of(out.dtype), stream.cuda_stream)
@@ -174,7 +176,9 @@ class LREPlan:
         (lre_validate_counts, records.py:34-56) on the same stream; the result
         is read by verify(), which raises the reference's message for the
         first bad setting — the streaming counterpart of validating a record
-        before the reconstruction."""
+        before the reconstruction.  An empty range is a no-op."""
+        if int(w_end) == int(w_begin):
+            return
         if validate:
             torch = _torch()
             res = torch.empty(3, dtype=torch.int64, device=self.device)
@@ -200,6 +204,8 @@ class LREPlan:
         """Streaming ingestion of an outcome-list chunk: histogram on the device, then stage."""
         torch = _torch()
         rows = int(outcomes.shape[0])
+        if rows == 0:
+            return
         buf = getattr(self, "_dense", None)
         if buf is None or buf.shape[0] < rows:
             dt = _torch_count_dtype(compact_dtype(self.shots))
