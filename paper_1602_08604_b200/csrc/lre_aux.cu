@@ -4,6 +4,8 @@
 #include <climits>
 #include <cmath>
 
+#include <type_traits>
+
 #include "lre_internal.cuh"
 
 namespace lre {
@@ -13,19 +15,36 @@ namespace lre {
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void validate_kernel(const T *__restrict__ counts, int n, int64_t rows, int64_t shots,
-                                long long *__restrict__ result) {
+                                long long *__restrict__ result, bool aligned16) {
     const int64_t d = (int64_t)1 << n;
     const int lane = threadIdx.x & 31;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     long long local_min = LLONG_MAX;
+    constexpr int VE = 16 / sizeof(T);  // elements per 16-byte load
+    const bool vec = aligned16 && (d % (32 * VE)) == 0;  // whole rows of 512-byte warp loads
     for (int64_t r = warp; r < rows; r += nwarps) {
         const T *row = counts + r * d;
         long long s = 0;
-        for (int64_t j = lane; j < d; j += 32) {
-            const long long v = (long long)row[j];
-            s += v;
-            local_min = v < local_min ? v : local_min;
+        if (vec) {
+            const uint4 *row4 = reinterpret_cast<const uint4 *>(row);
+            for (int64_t j = lane; j < d / VE; j += 32) {
+                const uint4 q = __ldcs(row4 + j);
+                const T *e = reinterpret_cast<const T *>(&q);
+#pragma unroll
+                for (int k = 0; k < VE; ++k) {
+                    const long long v = (long long)e[k];
+                    s += v;
+                    if constexpr (std::is_signed<T>::value) local_min = v < local_min ? v : local_min;
+                }
+            }
+            if constexpr (!std::is_signed<T>::value) local_min = 0;  // unsigned counts are never negative
+        } else {
+            for (int64_t j = lane; j < d; j += 32) {
+                const long long v = (long long)row[j];
+                s += v;
+                local_min = v < local_min ? v : local_min;
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -70,8 +89,9 @@ static int validate_t(const void *counts, int n, int64_t rows, int64_t shots, in
     init_result_kernel<<<1, 1, 0, s>>>(res);
     const int64_t warps_needed = rows;
     const int64_t blocks = std::min<int64_t>((warps_needed + 7) / 8, 148 * 32);
+    const bool aligned16 = (reinterpret_cast<uintptr_t>(counts) & 15) == 0;
     validate_kernel<T><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(reinterpret_cast<const T *>(counts), n,
-                                                                              rows, shots, res);
+                                                                              rows, shots, res, aligned16);
     row_sum_kernel<T><<<1, 256, 0, s>>>(reinterpret_cast<const T *>(counts), n, res);
     count_launch(3);
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
