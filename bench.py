@@ -224,7 +224,7 @@ class MuPipe:
         b = self.k % 2
         comp.wait_event(self.done[b])  # the previous copy-out of this buffer has finished
         d = 1 << self.plan.n
-        self.lib.call("lre_assemble", self.plan.theta.data_ptr(), self.lib.NATURAL, self.plan.n, 0, d,
+        self.lib.call("lre_assemble", self.plan.theta.data_ptr(), self.plan.layout, self.plan.n, 0, d,
                       self.dev[b].data_ptr(), comp.cuda_stream)
         ready = self.torch.cuda.Event()
         ready.record(comp)

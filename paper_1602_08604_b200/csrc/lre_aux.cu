@@ -88,7 +88,7 @@ static int validate_t(const void *counts, int n, int64_t rows, int64_t shots, in
     long long *res = reinterpret_cast<long long *>(result);
     init_result_kernel<<<1, 1, 0, s>>>(res);
     const int64_t warps_needed = rows;
-    const int64_t blocks = std::min<int64_t>((warps_needed + 7) / 8, 148 * 32);
+    const int64_t blocks = std::min<int64_t>((warps_needed + 7) / 8, (int64_t)num_sms() * 32);
     const bool aligned16 = (reinterpret_cast<uintptr_t>(counts) & 15) == 0;
     validate_kernel<T><<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, s>>>(reinterpret_cast<const T *>(counts), n,
                                                                               rows, shots, res, aligned16);
@@ -111,8 +111,11 @@ int validate_impl(const void *counts, int dtype, int n, int64_t rows, int64_t sh
 // ---------------------------------------------------------------------------
 // finalisation: exact numerators -> theta (pipeline.py:138, records.py:62-64)
 // ---------------------------------------------------------------------------
-__global__ void finalize_kernel(const int64_t *__restrict__ num, int n, int64_t shots,
-                                int layout, int64_t begin, int64_t end, double scale, double *__restrict__ theta) {
+__global__ void finalize_kernel(const int64_t *__restrict__ num, int n, int layout, int64_t begin, int64_t end,
+                                const Factors fac, double *__restrict__ theta) {
+    __shared__ double sfac[33];
+    stage_factors(sfac, fac);
+    __syncthreads();
     for (int64_t pos = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pos < end;
          pos += (int64_t)gridDim.x * blockDim.x) {
         uint32_t m, a;
@@ -123,7 +126,8 @@ __global__ void finalize_kernel(const int64_t *__restrict__ num, int n, int64_t 
             natural_to_ma((uint64_t)pos, m, a);
         }
         const int zc = n - __popc(m | a);
-        theta[pos - begin] = ((double)num[pos - begin] / (double)shots) * scale / pow3d(zc);
+        // the same epilogue as the last fold pass of lre_step1 (bit-identical theta)
+        theta[pos - begin] = (double)num[pos - begin] * sfac[zc];
     }
 }
 
@@ -131,9 +135,8 @@ int finalize_impl(const int64_t *num, int n, int64_t shots, int layout, int64_t 
                   cudaStream_t s) {
     if (end < begin) return LRE_EINVAL;
     if (end == begin) return LRE_OK;
-    const int64_t blocks = std::min<int64_t>((end - begin + 255) / 256, 148 * 16);
-    finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(num, n, shots, layout, begin, end, pow(2.0, -n / 2.0),
-                                                     theta);
+    const int64_t blocks = std::min<int64_t>((end - begin + 255) / 256, (int64_t)num_sms() * 16);
+    finalize_kernel<<<(unsigned)blocks, 256, 0, s>>>(num, n, layout, begin, end, make_factors(n, shots), theta);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
 }
@@ -160,7 +163,7 @@ __global__ void relayout_kernel(const double *__restrict__ src, int src_layout, 
 
 int relayout_impl(const double *src, int src_layout, int n, double *dst, cudaStream_t s) {
     const int64_t total = (int64_t)1 << (2 * n);
-    const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
     relayout_kernel<<<(unsigned)blocks, 256, 0, s>>>(src, src_layout, n, dst);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;

@@ -141,23 +141,13 @@ __global__ void __launch_bounds__(DENSE_THREADS) gen_theta_kernel(const double *
     }
 }
 
-static int num_sms_dense() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return sms;
-}
-
 int dense_to_theta_impl(const double *rho, int n, double *theta, cudaStream_t s) {
     if (n < 1 || n > 12) return LRE_EUNSUPPORTED;
     const size_t smem = 2 * ((size_t)1 << n) * sizeof(double);
     if (cudaFuncSetAttribute(dense_to_theta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
         return LRE_ECUDA;
-    const int grid = (int)std::min<int64_t>((int64_t)1 << n, (int64_t)num_sms_dense() * 4);
+    const int grid = (int)std::min<int64_t>((int64_t)1 << n, (int64_t)num_sms() * 4);
     dense_to_theta_kernel<<<grid, DENSE_THREADS, smem, s>>>(reinterpret_cast<const double2 *>(rho), n, theta);
     count_launch(1);
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
@@ -171,7 +161,7 @@ static int gen_theta_t(const double *theta, int n, int64_t shots, uint64_t seed,
         cudaSuccess)
         return LRE_ECUDA;
     const int64_t rows = w_end - w_begin;
-    const int grid = (int)std::min<int64_t>(rows, (int64_t)num_sms_dense() * 8);
+    const int grid = (int)std::min<int64_t>(rows, (int64_t)num_sms() * 8);
     gen_theta_kernel<T><<<grid, DENSE_THREADS, smem, s>>>(theta, n, shots, seed, w_begin, w_end,
                                                            reinterpret_cast<T *>(out));
     count_launch(1);

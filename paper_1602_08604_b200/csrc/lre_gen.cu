@@ -203,7 +203,7 @@ static int gen_t(int kind, int n, int64_t bits, int64_t shots, uint64_t seed, in
                  void *out, cudaStream_t s) {
     const int64_t rows = w_end - w_begin;
     if (rows <= 0) return LRE_OK;
-    const unsigned blocks = (unsigned)std::min<int64_t>(rows, 148 * 16);
+    const unsigned blocks = (unsigned)std::min<int64_t>(rows, (int64_t)num_sms() * 16);
     if (exact) {
         int *err = nullptr;
         if (cudaMallocAsync(&err, sizeof(int), s) != cudaSuccess) return LRE_ECUDA;
@@ -230,7 +230,7 @@ int generate_outcomes_impl(int kind, int n, int64_t bits, int64_t shots, uint64_
     if (kind < LRE_STATE_MAXMIXED || kind > LRE_STATE_W || shots < 1) return LRE_EINVAL;
     const int64_t rows = w_end - w_begin;
     if (rows <= 0) return LRE_OK;
-    const unsigned blocks = (unsigned)std::min<int64_t>(rows, 148 * 16);
+    const unsigned blocks = (unsigned)std::min<int64_t>(rows, (int64_t)num_sms() * 16);
     gen_outcomes_kernel<<<blocks, 256, 0, s>>>(kind, n, bits, shots, seed, w_begin, w_end, out);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
@@ -242,9 +242,7 @@ static int hist_t(const uint16_t *outcomes, int n, int64_t shots, int64_t rows, 
     cudaError_t e = cudaFuncSetAttribute(counts_from_outcomes_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return LRE_ECUDA;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = num_sms();
     const int per_sm = std::max(1, std::min(4, (int)((200 * 1024) / smem)));
     const unsigned blocks = (unsigned)std::min<int64_t>(rows, (int64_t)sms * per_sm);
     counts_from_outcomes_kernel<T><<<blocks, 512, smem, s>>>(outcomes, n, shots, rows, reinterpret_cast<T *>(counts));

@@ -2,6 +2,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
 #include <stdint.h>
 
 #include "../../include/lre_b200.h"
@@ -16,6 +18,9 @@ __host__ __device__ constexpr int popc_c(int x) { return x == 0 ? 0 : (x & 1) + 
 
 // global launch counter (bench.py reports it as gpu_launches)
 void count_launch(int k = 1);
+
+// multiprocessor count of the current device (grid sizing; cached per device)
+int num_sms();
 
 // Philox4x32-10 (counter-based): the record generators key it on (seed) with
 // counters (shot, ..., setting), so records do not depend on launch shape.
@@ -126,6 +131,90 @@ __device__ __forceinline__ uint64_t spread_bits(uint32_t x) {
 // (m, a) -> natural index: hi bit = a, lo bit = a ^ m
 __device__ __forceinline__ uint64_t ma_to_natural(uint32_t m, uint32_t a) {
     return (spread_bits(a) << 1) | spread_bits(a ^ m);
+}
+
+// Epilogue factors theta = N * fac[zc], fac[zc] = 2^{-n/2} / shots / 3^zc
+// (pipeline.py:138, records.py:62-64) rounded once from the long-double
+// quotient: one multiply per output instead of two fp64 divisions (relative
+// error <= 2 ulp, the int64 numerators N stay exact).  Every kernel that
+// finishes numerators (the last fold pass, lre_finalize) takes the table by
+// value and stages it in shared memory (lanes of a warp index different zc;
+// divergent constant-bank reads would serialise), so results are bit-identical
+// across entry points and the library keeps no per-(n, shots) device state.
+struct Factors {
+    double f[33];
+};
+inline Factors make_factors(int n, int64_t shots) {
+    Factors fac;
+    const long double scale = (long double)pow(2.0, -n / 2.0);
+    long double p3 = 1.0L;
+    for (int zc = 0; zc < 33; ++zc) {
+        fac.f[zc] = (double)(scale / (long double)shots / p3);
+        p3 *= 3.0L;
+    }
+    return fac;
+}
+// copy the table into shared memory; the caller synchronises before use
+__device__ __forceinline__ void stage_factors(double *dst, const Factors &fac) {
+    for (int i = threadIdx.x; i < 33; i += blockDim.x) dst[i] = fac.f[i];
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier / bulk-copy (TMA) helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+#ifdef LRE_MBAR_WATCHDOG
+    // debug builds: trap (instead of hanging) when a phase never completes
+    for (long long it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == (1ll << 22)) {
+            if ((threadIdx.x & 31) == 0)
+                printf("LRE mbarrier watchdog: block %d thread %d bar %p parity %u\n", blockIdx.x, threadIdx.x, bar,
+                       parity);
+            __trap();
+        }
+    }
+#endif
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LRE_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra LRE_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> this CTA's shared memory, completing on `bar`
+// (size a multiple of 16 bytes)
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// order this thread's generic-proxy shared-memory accesses before later async-proxy (TMA) ones
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
 // 3^k as an exact double (k <= 32)

@@ -37,15 +37,6 @@
 
 namespace lre {
 
-// theta = N * g_fac[zc], g_fac[zc] = 2^{-n/2} / shots / 3^zc (set per launch
-// sequence): one multiply per output instead of two fp64 divisions; relative
-// error <= 2 ulp, far inside the 1e-10 parity bar (the integer numerators
-// N stay exact).
-// (global memory, read with __ldg: lanes of a warp use different zc, and
-// divergent __constant__ reads serialise — that alone made the final pass 2.4x
-// slower than its bytes)
-__device__ double g_fac[33];
-
 // ===========================================================================
 // epilogue shared by both kernels
 // ===========================================================================
@@ -57,11 +48,11 @@ struct Final {
     int layout;  // LRE_LAYOUT_* (final outputs only)
     int n;
     int64_t shots;
-    double scale;  // 2^{-n/2}
+    Factors fac;  // theta = N * fac[zc] (lre_internal.cuh), staged in shared memory by the final kernels
 };
 
-// store a finished numerator at natural Pauli index `nat`
-__device__ __forceinline__ void store_final(const Final &f, uint64_t nat, int64_t v) {
+// store a finished numerator at natural Pauli index `nat`; sfac = the staged fac table
+__device__ __forceinline__ void store_final(const Final &f, const double *sfac, uint64_t nat, int64_t v) {
     uint64_t pos = nat;
     if (f.layout == LRE_LAYOUT_MASK_MAJOR) {
         uint32_t m, a;
@@ -73,7 +64,7 @@ __device__ __forceinline__ void store_final(const Final &f, uint64_t nat, int64_
     } else {
         // zc = number of I (zero) base-4 digits of the natural index
         const int zc = f.n - __popcll((nat | (nat >> 1)) & 0x5555555555555555ull);
-        reinterpret_cast<double *>(f.out)[pos] = (double)v * __ldg(&g_fac[zc]);
+        reinterpret_cast<double *>(f.out)[pos] = (double)v * sfac[zc];
     }
 }
 
@@ -312,10 +303,14 @@ __device__ __forceinline__ void l2_transform(const T *st, Sink sink) {
     sink(0, Iacc);
 }
 
-// int32 numerators in natural order -> final theta / int64 numerators
-__global__ void __launch_bounds__(256) convert_kernel(const int32_t *__restrict__ in, int64_t count, const Final f) {
+// numerators (int32 or int64) in natural order -> final theta / int64 numerators
+template <typename Tn>
+__global__ void __launch_bounds__(256) convert_kernel(const Tn *__restrict__ in, int64_t count, const Final f) {
+    __shared__ double sfac[33];
+    stage_factors(sfac, f.fac);
+    __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
-        store_final(f, (uint64_t)i, (int64_t)in[i]);
+        store_final(f, sfac, (uint64_t)i, (int64_t)in[i]);
 }
 
 // Staged record of one L1 item: 64 values (+ padding) at position
@@ -795,45 +790,6 @@ template <int Q> struct TmaSmem {
     static constexpr size_t TOTAL = 1024 /* alignment slack */ + RING + 2 * STAGE + EXTRA + BARS;
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-#ifdef LRE_MBAR_WATCHDOG
-    // debug builds: trap (instead of hanging) when a phase never completes
-    for (long long it = 0;; ++it) {
-        uint32_t ok;
-        asm volatile(
-            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (ok) return;
-        if (it == (1ll << 22)) {
-            if ((threadIdx.x & 31) == 0 || threadIdx.x >= TMA_COMPUTE_THREADS)
-                printf("LRE mbarrier watchdog: block %d thread %d bar %p parity %u\n", blockIdx.x, threadIdx.x, bar,
-                       parity);
-            __trap();
-        }
-    }
-#endif
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "LRE_WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra LRE_WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -1027,6 +983,11 @@ __global__ void __launch_bounds__(128, Q == 1 ? VF1_MINB : 4) vfold_kernel(const
     constexpr int RL = R3 / 3;  // rows per top digit
     const int64_t total = a.nA * a.nB * a.V;
     const Tin *in = reinterpret_cast<const Tin *>(a.in);
+    __shared__ double sfac[FINAL ? 33 : 1];
+    if constexpr (FINAL) {
+        stage_factors(sfac, a.f.fac);
+        __syncthreads();
+    }
     if (Q == 1 && a.vf1_batch) {
         // One qubit: each thread issues the six row loads of VF1_U elements
         // before any arithmetic (the r1-streamed vblock keeps only two loads
@@ -1068,7 +1029,7 @@ __global__ void __launch_bounds__(128, Q == 1 ? VF1_MINB : 4) vfold_kernel(const
                     for (int d = 0; d < 4; ++d) out[(int64_t)d * a.V] = D[d];
                 } else {
 #pragma unroll
-                    for (int d = 0; d < 4; ++d) store_final(a.f, (uint64_t)(d * a.V + vv[u]), (int64_t)D[d]);
+                    for (int d = 0; d < 4; ++d) store_final(a.f, sfac, (uint64_t)(d * a.V + vv[u]), (int64_t)D[d]);
                 }
             }
         }
@@ -1092,7 +1053,7 @@ __global__ void __launch_bounds__(128, Q == 1 ? VF1_MINB : 4) vfold_kernel(const
             Ta *out = reinterpret_cast<Ta *>(a.f.out) + ((A - a.ya0) * a.nB + B) * NOUT * V + v;
             vblock<Q, Ta>(ld, [&](int d, Ta y) { out[(int64_t)d * V] = y; });
         } else {
-            vblock<Q, Ta>(ld, [&](int d, Ta y) { store_final(a.f, (uint64_t)(d * V + v), (int64_t)y); });
+            vblock<Q, Ta>(ld, [&](int d, Ta y) { store_final(a.f, sfac, (uint64_t)(d * V + v), (int64_t)y); });
         }
     }
     }
@@ -1126,6 +1087,11 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const 
     extern __shared__ __align__(16) int4 vsm4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int4 *ring = vsm4 + warp * VF3_SLOTS * VF3_GROUP_CHUNKS;
+    __shared__ double sfac[FINAL ? 33 : 1];
+    if constexpr (FINAL) {
+        stage_factors(sfac, a.f.fac);
+        __syncthreads();
+    }
     const int64_t V = a.V;
     const int64_t nvb = V >> 5;
     const int64_t ntask = a.nA * a.nB * nvb;
@@ -1178,7 +1144,7 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const 
         if constexpr (!FINAL) out = reinterpret_cast<int32_t *>(a.f.out) + ((A - a.ya0) * a.nB + B) * 64 * V + v;
         auto sink = [&](int d, int32_t y) {
             if constexpr (!FINAL) out[(int64_t)d * V] = y;
-            else store_final(a.f, (uint64_t)(d * V + v), (int64_t)y);
+            else store_final(a.f, sfac, (uint64_t)(d * V + v), (int64_t)y);
         };
         if (r1 == 0) {
 #pragma unroll
@@ -1244,6 +1210,13 @@ struct Pass {
     size_t out_bytes; // intermediate output bytes (0 for the final pass)
 };
 
+// byte offset of the int64 numerators a one-pass streaming stage leaves in the workspace
+static inline size_t onepass_num_offset(int n) {
+    size_t b = 1;
+    for (int i = 0; i < n; ++i) b *= 4;
+    return (b * sizeof(int32_t) + 255) & ~(size_t)255;
+}
+
 struct Plan {
     std::vector<Pass> p;
     size_t ws_bytes = 0;
@@ -1308,11 +1281,12 @@ Plan make_plan(int n, int64_t shots, int dtype, int64_t w_begin, int64_t w_end) 
     pl.off[0] = 0;
     pl.off[1] = (need[0] + 255) & ~(size_t)255;
     pl.ws_bytes = pl.off[1] + ((need[1] + 255) & ~(size_t)255);
-    if (pl.p.size() == 1 && pl.p[0].kind == 0) pl.ws_bytes = (size_t)ipow(4, n) * sizeof(int32_t);
+    // one-pass plans (n <= 2, 6, 7): int32 tile of the tile pass, then (streaming
+    // form only) the int64 numerators that lre_step1_stage leaves for _finish
+    if (pl.p.size() == 1) pl.ws_bytes = onepass_num_offset(n) + (size_t)ipow(4, n) * sizeof(int64_t);
     return pl;
 }
 
-static int g_num_sms = 0;
 static bool g_pow3_ready = false;
 
 static bool g_disable_tma;
@@ -1325,12 +1299,6 @@ static cudaError_t ensure_init() {
         g_disable_tma = g_p1_variant != 2;
         g_pow3_ready = true;
     }
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaError_t e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e != cudaSuccess) return e;
-    }
     return cudaSuccess;
 }
 
@@ -1341,7 +1309,7 @@ static cudaError_t launch_tile(const P1Args &a, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = a.naH * a.C;
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * (SMALL ? 2 : 1));  // persistent
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms() * (SMALL ? 2 : 1));  // persistent
     kern<<<(unsigned)grid, P1_THREADS, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
@@ -1354,7 +1322,7 @@ static cudaError_t launch_ring(const P1Args &a, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = a.naH * a.C;
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms);
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms());
     kern<<<(unsigned)grid, RING_THREADS, smem, s>>>(a);
     count_launch();
     return cudaGetLastError();
@@ -1429,7 +1397,7 @@ static cudaError_t launch_tma(const P1Args &a, cudaStream_t s) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = a.naH * a.C;
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms);
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)num_sms());
     kern<<<(unsigned)grid, TMA_THREADS, smem, s>>>(a, map);
     count_launch();
     return cudaGetLastError();
@@ -1455,7 +1423,7 @@ static cudaError_t run_tile(int q, int small, int dtype, const P1Args &a, cudaSt
 template <int Q, typename Tin, typename Ta>
 static cudaError_t launch_vfold(const VArgs &a, cudaStream_t s) {
     const int64_t total = a.nA * a.nB * a.V;
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 127) / 128, (int64_t)g_num_sms * 16));
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 127) / 128, (int64_t)num_sms() * 16));
     if (a.f.kind == OUT_INTER) vfold_kernel<Q, Tin, Ta, false><<<(unsigned)blocks, 128, 0, s>>>(a);
     else vfold_kernel<Q, Tin, Ta, true><<<(unsigned)blocks, 128, 0, s>>>(a);
     count_launch();
@@ -1466,7 +1434,7 @@ static cudaError_t launch_vfold3(const VArgs &a, cudaStream_t s) {
     const size_t smem = (size_t)VF3_WARPS * VF3_SLOTS * VF3_GROUP_CHUNKS * sizeof(int4);
     const int64_t tasks = a.nA * a.nB * (a.V >> 5);
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((tasks + VF3_WARPS - 1) / VF3_WARPS,
-                                                                (int64_t)g_num_sms * VF3_MINB));
+                                                                (int64_t)num_sms() * VF3_MINB));
     cudaError_t e;
     if (a.f.kind == OUT_INTER) {
         e = cudaFuncSetAttribute(vfold3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1495,6 +1463,95 @@ static cudaError_t vfold_q(int q, const VArgs &a, cudaStream_t s) {
     }
 }
 
+// Last fold pass (one qubit: the most significant) writing MASK_MAJOR output
+// (theta[m * 2^n + a], the layout the n >= 10 assembly bulk-copies mask by
+// mask).  Natural digits interleave the m and a bits, so a lane-per-element
+// store would scatter 8-byte writes over 2^n-strided mask rows.  A block takes
+// 1024 consecutive v (the five lowest qubits complete): (m5, a5) =
+// natural_to_ma(v & 1023) covers a full 32 x 32 grid, so after staging the
+// 4 x 1024 results in shared memory as [digit][m5][a5] every warp writes runs
+// of 32 consecutive doubles (256 B) of one mask row.  Reads: the six
+// (setting digit, outcome bit) planes of the input, 4 KB lines.
+template <typename Tin, typename Ta, bool NUM>
+__global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
+    __shared__ double st[4 * 32 * 33];
+    __shared__ double sfac[33];
+    if constexpr (!NUM) stage_factors(sfac, a.f.fac);
+    const Tin *in = reinterpret_cast<const Tin *>(a.in);
+    const int n = a.f.n;
+    const int64_t V = a.V;  // 4^(n-1)
+    const int64_t nblk = V >> 10;
+    const int64_t rstride = a.ncol * V;
+    __syncthreads();
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t v0 = blk << 10;
+        uint32_t mh, ah;  // mask / a bits of qubits 2 .. n-5 (natural_to_ma of the block index)
+        natural_to_ma((uint64_t)blk, mh, ah);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int vl = threadIdx.x + 256 * k;
+            Ta x[6];
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const int64_t row = r;
+                    x[2 * r + b] = (row >= a.alo && row < a.ahi)
+                                       ? (Ta)vload<Tin>(in + (row - a.xa0) * rstride + (int64_t)b * V + v0 + vl)
+                                       : (Ta)0;
+                }
+            const Ta D[4] = {(x[0] + x[1]) + (x[2] + x[3]) + (x[4] + x[5]), x[0] - x[1], x[2] - x[3], x[4] - x[5]};
+            uint32_t m5, a5;
+            natural_to_ma((uint64_t)vl, m5, a5);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) {
+                double val;
+                if constexpr (NUM) {
+                    val = __longlong_as_double((long long)D[d]);
+                } else {
+                    const uint32_t mt = (d == 1 || d == 2), at = (d >= 2);
+                    const uint32_t mfull = (mt << (n - 1)) | (mh << 5) | m5, afull = (at << (n - 1)) | (ah << 5) | a5;
+                    val = (double)D[d] * sfac[n - __popc(mfull | afull)];
+                }
+                st[(d * 32 + m5) * 33 + a5] = val;
+            }
+        }
+        __syncthreads();
+        // 128 rows (digit, m5) of 32 doubles: warp w writes rows w, w + 8, ...
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll 4
+        for (int row = warp; row < 128; row += 8) {
+            const int d = row >> 5, m5 = row & 31;
+            const uint64_t mt = (d == 1 || d == 2), at = (d >= 2);
+            const uint64_t m = (mt << (n - 1)) | ((uint64_t)mh << 5) | (uint64_t)m5;
+            const uint64_t aa = (at << (n - 1)) | ((uint64_t)ah << 5) | (uint64_t)lane;
+            const double val = st[row * 33 + lane];
+            const uint64_t pos = (m << n) | aa;
+            if constexpr (NUM) reinterpret_cast<int64_t *>(a.f.out)[pos] = (int64_t)__double_as_longlong(val);
+            else __stcs(reinterpret_cast<double *>(a.f.out) + pos, val);
+        }
+        __syncthreads();
+    }
+}
+
+static cudaError_t launch_final_mm(int in_dtype, int acc64, const VArgs &a, cudaStream_t s) {
+    const int64_t nblk = a.V >> 10;
+    const unsigned grid = (unsigned)std::min<int64_t>(nblk, (int64_t)num_sms() * 8);
+    const bool num = a.f.kind == OUT_NUM;
+#define LRE_FMM(TIN, TA)                                                                  \
+    do {                                                                                  \
+        if (num) final_mm_kernel<TIN, TA, true><<<grid, 256, 0, s>>>(a);                  \
+        else final_mm_kernel<TIN, TA, false><<<grid, 256, 0, s>>>(a);                     \
+    } while (0)
+    if (in_dtype == LRE_I32 && acc64) LRE_FMM(int32_t, int64_t);
+    else if (in_dtype == LRE_I32) LRE_FMM(int32_t, int32_t);
+    else if (in_dtype == LRE_I64) LRE_FMM(int64_t, int64_t);
+    else return cudaErrorInvalidValue;
+#undef LRE_FMM
+    count_launch();
+    return cudaGetLastError();
+}
+
 static cudaError_t run_vfold(int q, int in_dtype, int acc64, const VArgs &a, cudaStream_t s) {
 #ifdef LRE_ONLY_ONE
     return vfold_q<int32_t, int32_t>(q, a, s);
@@ -1519,36 +1576,11 @@ static cudaError_t run_vfold(int q, int in_dtype, int acc64, const VArgs &a, cud
 
 // Run passes [first, last) of `pl` (computed rows) with intermediates laid out
 // as in `lay` (== pl for one-shot shards; the full-range plan for streaming).
-static int g_fac_n = -1, g_fac_dev = -1;
-static int64_t g_fac_shots = -1;
-
-// g_fac for (n, shots); uploaded only when they change (stream-ordered)
-static cudaError_t set_factors(int n, int64_t shots, cudaStream_t s) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (n == g_fac_n && shots == g_fac_shots && dev == g_fac_dev) return cudaSuccess;
-    static double fac[33];
-    const double scale = pow(2.0, -n / 2.0);
-    double p3 = 1.0;
-    for (int zc = 0; zc < 33; ++zc) {
-        fac[zc] = (double)((long double)scale / (long double)shots / (long double)p3);
-        p3 *= 3.0;
-    }
-    cudaError_t e = cudaMemcpyToSymbolAsync(g_fac, fac, sizeof(fac), 0, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return e;
-    e = cudaStreamSynchronize(s);  // fac[] is static host memory reused by the next call
-    if (e != cudaSuccess) return e;
-    g_fac_n = n;
-    g_fac_shots = shots;
-    g_fac_dev = dev;
-    return cudaSuccess;
-}
-
 static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last, const void *counts,
                       int64_t row_base, int n, int64_t shots, void *ws, void *out, int out_kind, int layout,
                       cudaStream_t stream) {
     if (ensure_init() != cudaSuccess) return LRE_ECUDA;
-    if (last == pl.p.size() && set_factors(n, shots, stream) != cudaSuccess) return LRE_ECUDA;
+    const Factors fac = make_factors(n, shots);
     int done = 0;
     for (size_t i = 0; i < first; ++i) done += pl.p[i].q;
     for (size_t i = first; i < last; ++i) {
@@ -1562,7 +1594,7 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
         f.layout = layout;
         f.n = n;
         f.shots = shots;
-        f.scale = pow(2.0, -n / 2.0);
+        f.fac = fac;
         const void *in = i == 0 ? counts : (const void *)((const char *)ws + lay.off[(i - 1) & 1]);
         cudaError_t e;
         if (ps.kind == 0) {
@@ -1586,8 +1618,8 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             e = run_tile(ps.q, ps.small, ps.in_dtype, a, stream);
             if (e == cudaSuccess && fin) {
                 const int64_t count = ipow(4, n);
-                const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)g_num_sms * 8);
-                convert_kernel<<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const int32_t *>(ws), count, f);
+                const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 8);
+                convert_kernel<int32_t><<<(unsigned)blocks, 256, 0, stream>>>(reinterpret_cast<const int32_t *>(ws), count, f);
                 count_launch();
                 e = cudaGetLastError();
             }
@@ -1611,7 +1643,9 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             }();
             a.vf1_batch = vf1;
             a.f = f;
-            e = run_vfold(ps.q, ps.in_dtype, ps.acc64, a, stream);
+            const bool fmm = fin && ps.q == 1 && layout == LRE_LAYOUT_MASK_MAJOR && a.V >= 1024 && a.A0 == 0 && a.nA == 1 &&
+                             a.nB == 1 && (ps.in_dtype == LRE_I32 || ps.in_dtype == LRE_I64);
+            e = fmm ? launch_final_mm(ps.in_dtype, ps.acc64, a, stream) : run_vfold(ps.q, ps.in_dtype, ps.acc64, a, stream);
         }
         if (e != cudaSuccess) return e == cudaErrorInvalidValue ? LRE_EUNSUPPORTED : LRE_ECUDA;
         done += ps.q;
@@ -1626,12 +1660,19 @@ int step1_impl(const void *counts, int dtype, int n, int64_t shots, int64_t w_be
     return run_passes(pl, pl, 0, pl.p.size(), counts, w_begin, n, shots, ws, out, out_kind, layout, stream);
 }
 
-// pass 1 of a setting chunk into the full-range workspace (streaming records)
+// pass 1 of a setting chunk into the full-range workspace (streaming records).
+// A one-pass plan (n <= 2, 6, 7) has a shard quantum equal to the whole
+// record, so its only chunk is [0, 3^n): stage computes the exact int64
+// numerators into the workspace and finish converts them.
 int step1_stage_impl(const void *counts, int dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end, void *ws,
                      size_t ws_bytes, cudaStream_t stream) {
     const Plan full = make_plan(n, shots, dtype, 0, ipow(3, n));
-    if (full.p.size() < 2) return LRE_EUNSUPPORTED;
     if (ws_bytes < full.ws_bytes || !ws) return LRE_ENOMEM;
+    if (full.p.size() < 2) {
+        if (w_begin != 0 || w_end != ipow(3, n)) return LRE_EINVAL;
+        return run_passes(full, full, 0, 1, counts, 0, n, shots, ws, (char *)ws + onepass_num_offset(n),
+                          LRE_OUT_NUM_I64, LRE_LAYOUT_NATURAL, stream);
+    }
     const Plan pl = make_plan(n, shots, dtype, w_begin, w_end);
     return run_passes(pl, full, 0, 1, counts, w_begin, n, shots, ws, nullptr, 0, 0, stream);
 }
@@ -1641,8 +1682,23 @@ int step1_finish_impl(void *ws, size_t ws_bytes, int n, int64_t shots, void *out
                       cudaStream_t stream) {
     // the count dtype only affects pass 1; any value gives the same later passes
     const Plan full = make_plan(n, shots, LRE_I64, 0, ipow(3, n));
-    if (full.p.size() < 2) return LRE_EUNSUPPORTED;
     if (ws_bytes < full.ws_bytes || !ws) return LRE_ENOMEM;
+    if (ensure_init() != cudaSuccess) return LRE_ECUDA;
+    if (full.p.size() < 2) {
+        Final f;
+        f.kind = out_kind == LRE_OUT_NUM_I64 ? OUT_NUM : OUT_THETA;
+        f.out = out;
+        f.layout = layout;
+        f.n = n;
+        f.shots = shots;
+        f.fac = make_factors(n, shots);
+        const int64_t count = ipow(4, n);
+        const int64_t blocks = std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 8);
+        convert_kernel<int64_t><<<(unsigned)blocks, 256, 0, stream>>>(
+            reinterpret_cast<const int64_t *>((const char *)ws + onepass_num_offset(n)), count, f);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
+    }
     return run_passes(full, full, 1, full.p.size(), nullptr, 0, n, shots, ws, out, out_kind, layout, stream);
 }
 

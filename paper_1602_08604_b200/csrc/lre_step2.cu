@@ -265,17 +265,275 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) assemble_pair
     }
 }
 
+// ---------------------------------------------------------------------------
+// n >= 11, mask-major theta: assemble_cl8_kernel<LOGD>
+//
+// The write pattern decides this kernel (profiles/r02_microbench_mu_writes.txt,
+// 4.3 GB of XOR-diagonal stores at n = 14): a row segment of 16 B (one mask)
+// runs at 1.1 TB/s, 32 B (a mask pair) at 2.9-3.6 TB/s and 64 B at 2.9-4.7
+// TB/s depending on whether the CTAs writing the two halves of a 128-byte line
+// happen to be in step; only whole 128-byte lines (8 consecutive masks per
+// row) hold 4.6 TB/s for any schedule.  One mask's transform is 2^n doubles
+// (128 KB at n = 14), so 8 masks cannot share one SM:
+//   * a cluster of 8 CTAs owns an aligned block of 8 masks, CTA j the
+//     transform of mask m0 + j, in its own shared memory;
+//   * theta arrives mask-major (each mask's 2^n coefficients contiguous) by
+//     bulk copies (cp.async.bulk, mbarrier completion): the first half of the
+//     next mask is prefetched into a staging buffer while the current mask is
+//     written out, the second half lands in the transform buffer as soon as
+//     the partners have finished reading it;
+//   * the fp64 WHT runs in three shared-memory rounds (bits 5-9 with the sign
+//     twist, bits 0-4, bits 10..n-1), one pad double per 32 (conflict-free);
+//   * after one cluster barrier CTA c writes rows [c d/8, (c+1) d/8): per row
+//     16 transform values (two per mask, 14 of them read from the partners
+//     through distributed shared memory) -> one 128-byte segment.
+// ---------------------------------------------------------------------------
+template <int LOGD> struct Cl8 {
+    static constexpr int D = 1 << LOGD;
+    static constexpr int NT = D / 32;     // threads per CTA
+    static constexpr int FP = D + D / 32; // padded transform (doubles)
+    static constexpr int HALF = D / 2;    // prefetched first half (doubles)
+    static constexpr int FH = HALF + HALF / 32;  // linear landing offset of the second half inside F
+    static constexpr size_t SMEM = (size_t)(FP + HALF) * sizeof(double) + 2 * sizeof(uint64_t);
+    static constexpr uint32_t HALF_BYTES = (uint32_t)HALF * sizeof(double);
+};
+
+__device__ __forceinline__ int pad32(int x) { return x + (x >> 5); }
+
+struct Cl8Args {
+    const double *theta;  // mask-major slice: theta[(m - m_begin) * 2^n + a]
+    int64_t m_begin;
+    int64_t S;            // masks in the slice (power of two >= 8); mu rows are S complex wide
+    int64_t units;        // S / 8
+    double scale_half;
+    double2 *mu;
+};
+
+template <int LOGD>
+__device__ __forceinline__ void cl8_issue_half(const Cl8Args &a, int64_t u, int rank, int half, double *dst,
+                                               uint64_t *bar) {
+    using C = Cl8<LOGD>;
+    const double *src = a.theta + ((u * 8 + rank) << LOGD) + (int64_t)half * C::HALF;
+    constexpr uint32_t CHUNK = C::HALF_BYTES < 16384u ? C::HALF_BYTES : 16384u;
+    mbar_expect_tx(bar, C::HALF_BYTES);
+#pragma unroll 1
+    for (uint32_t off = 0; off < C::HALF_BYTES; off += CHUNK)
+        bulk_load(reinterpret_cast<char *>(dst) + off, reinterpret_cast<const char *>(src) + off, CHUNK, bar);
+}
+
+template <int LOGD>
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(Cl8<LOGD>::NT, LOGD >= 14 ? 1 : LOGD == 13 ? 2 : 4) assemble_cl8_kernel(const Cl8Args a) {
+    using C = Cl8<LOGD>;
+    constexpr int D = C::D, NT = C::NT;
+    extern __shared__ __align__(16) double cl8_smem[];
+    double *F = cl8_smem;
+    double *Sbuf = cl8_smem + C::FP;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(Sbuf + C::HALF);
+    uint64_t *barS = bars, *barF = bars + 1;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const int t = threadIdx.x;
+    const int64_t ncl = gridDim.x / 8;
+    const int64_t u0 = blockIdx.x / 8;
+    if (t == 0) {
+        mbar_init(barS, 1);
+        mbar_init(barF, 1);
+        fence_mbar_init();
+        if (u0 < a.units) {
+            cl8_issue_half<LOGD>(a, u0, rank, 0, Sbuf, barS);
+            cl8_issue_half<LOGD>(a, u0, rank, 1, F + C::FH, barF);
+        }
+    }
+    __syncthreads();
+    uint32_t parity = 0;
+    for (int64_t u = u0; u < a.units; u += ncl, parity ^= 1) {
+        const uint32_t m = (uint32_t)(a.m_begin + u * 8 + rank);  // this CTA's mask
+        // ---- round A: bits 5..9 (+ sign twist), read linear, write padded ----
+        {
+            const int g = t >> 5, l = t & 31;
+            const int base = g * 1024 + l;
+            const double *src = base < C::HALF ? Sbuf + base : F + C::FH + (base - C::HALF);
+            double v[32];
+            mbar_wait(base < C::HALF ? barS : barF, parity);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t av = (uint32_t)(base + 32 * j);
+                const double x = src[32 * j];
+                v[j] = ((__popc(av & m) >> 1) & 1) ? -x : x;
+            }
+#pragma unroll
+            for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    if (!(j & h)) {
+                        const double x = v[j], y = v[j + h];
+                        v[j] = x + y;
+                        v[j + h] = x - y;
+                    }
+            __syncthreads();  // every read of the second half (landed inside F) precedes the padded writes
+#pragma unroll
+            for (int j = 0; j < 32; ++j) F[pad32(base + 32 * j)] = v[j];
+        }
+        __syncthreads();
+        // the staging buffer is consumed: prefetch the first half of the next mask
+        if (t == 0 && u + ncl < a.units) {
+            fence_proxy_async_smem();
+            cl8_issue_half<LOGD>(a, u + ncl, rank, 0, Sbuf, barS);
+        }
+        // ---- round B: bits 0..4 (32 consecutive elements per thread) ----
+        {
+            double *b = F + 33 * t;
+            double v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = b[i];
+#pragma unroll
+            for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (!(i & h)) {
+                        const double x = v[i], y = v[i + h];
+                        v[i] = x + y;
+                        v[i + h] = x - y;
+                    }
+#pragma unroll
+            for (int i = 0; i < 32; ++i) b[i] = v[i];
+        }
+        __syncthreads();
+        // ---- round C: bits 10..LOGD-1 ----
+        if constexpr (LOGD > 10) {
+            constexpr int K = 1 << (LOGD - 10);
+#pragma unroll 1
+            for (int bse = t; bse < 1024; bse += NT) {
+                double v[K];
+#pragma unroll
+                for (int j = 0; j < K; ++j) v[j] = F[pad32(bse + 1024 * j)];
+#pragma unroll
+                for (int h = 1; h < K; h <<= 1)
+#pragma unroll
+                    for (int j = 0; j < K; ++j)
+                        if (!(j & h)) {
+                            const double x = v[j], y = v[j + h];
+                            v[j] = x + y;
+                            v[j + h] = x - y;
+                        }
+#pragma unroll
+                for (int j = 0; j < K; ++j) F[pad32(bse + 1024 * j)] = v[j];
+            }
+        }
+        // ---- all 8 transforms of the cluster complete and visible ----
+        cluster.sync();
+        // ---- write phase: rows [rank d/8, (rank+1) d/8), one 128-byte segment each ----
+        {
+            const uint32_t m0 = (uint32_t)(a.m_begin + u * 8);
+            const int64_t smask = a.S - 1;
+#pragma unroll 1
+            for (int k = 0; k < 4; k += 2) {
+                // loads: mask j uniform across the warp, lanes on consecutive rows -> each
+                // warp access reads one partner's shared memory contiguously
+                double2 o[2][8];  // [row][mask j]: mu[r, r ^ (m0 + j)]
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const double *Fj = cluster.map_shared_rank(F, j);
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const int r = rank * (D / 8) + t + NT * (k + q);
+                        const double f1 = Fj[pad32(r)], f2 = Fj[pad32(r ^ (int)(m0 + j))];
+                        o[q][j] = make_double2(a.scale_half * (f1 + f2), a.scale_half * (f2 - f1));
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int r = rank * (D / 8) + t + NT * (k + q);
+                    // column slot of mask j is (r & 7) ^ j: permute the register array by
+                    // XOR with r & 7 (three conditional swap stages)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b) {
+                        const bool sw = (r >> b) & 1;
+#pragma unroll
+                        for (int x = 0; x < 8; ++x)
+                            if (!(x & (1 << b))) {
+                                const double2 lo = o[q][x], hi = o[q][x | (1 << b)];
+                                o[q][x] = sw ? hi : lo;
+                                o[q][x | (1 << b)] = sw ? lo : hi;
+                            }
+                    }
+                    const int64_t cb = (int64_t)((uint32_t)r ^ m0) & smask & ~(int64_t)7;
+                    double2 *dst = a.mu + (int64_t)r * a.S + cb;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) st256_cs(dst + 2 * w, o[q][2 * w], o[q][2 * w + 1]);
+                }
+            }
+        }
+        // partners have finished reading this CTA's transform (their loads were consumed by stores)
+        cluster_sync_relaxed();
+        if (t == 0 && u + ncl < a.units) {
+            fence_proxy_async_smem();
+            cl8_issue_half<LOGD>(a, u + ncl, rank, 1, F + C::FH, barF);
+        }
+    }
+}
+
+template <int LOGD>
+static int launch_cl8(const double *theta, int64_t m_begin, int64_t S, double *mu, cudaStream_t s) {
+    using C = Cl8<LOGD>;
+    auto kern = assemble_cl8_kernel<LOGD>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
+        return LRE_ECUDA;
+    Cl8Args a;
+    a.theta = theta;
+    a.m_begin = m_begin;
+    a.S = S;
+    a.units = S / 8;
+    a.scale_half = 0.5 * pow(2.0, -LOGD / 2.0);
+    a.mu = reinterpret_cast<double2 *>(mu);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(8, 1, 1);
+    cfg.blockDim = dim3(C::NT, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 8;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int max_clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, (void *)kern, &cfg) != cudaSuccess || max_clusters < 1)
+        max_clusters = std::max(1, num_sms() / 8);
+    const int64_t clusters = std::min<int64_t>(a.units, max_clusters);
+    kern<<<(unsigned)(8 * clusters), C::NT, C::SMEM, s>>>(a);
+    count_launch();
+    return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
+}
+
+// the cluster kernel applies to mask-major slices of >= 8 masks at n >= 11 (one
+// round-A group of 1024 coefficients must lie inside one half of a mask)
+// (LRE_ASM=legacy selects the round-1 kernels for A/B runs)
+static bool use_cl8(int layout, int n, int64_t S) {
+    static const bool legacy = [] {
+        const char *v = getenv("LRE_ASM");
+        return v && !strcmp(v, "legacy");
+    }();
+    return !legacy && layout == LRE_LAYOUT_MASK_MAJOR && n >= 11 && n <= 14 && S >= 8;
+}
+
+static int launch_cl8_n(int n, const double *theta, int64_t m_begin, int64_t S, double *mu, cudaStream_t s) {
+    switch (n) {
+    case 11: return launch_cl8<11>(theta, m_begin, S, mu, s);
+    case 12: return launch_cl8<12>(theta, m_begin, S, mu, s);
+    case 13: return launch_cl8<13>(theta, m_begin, S, mu, s);
+    case 14: return launch_cl8<14>(theta, m_begin, S, mu, s);
+    default: return LRE_EUNSUPPORTED;
+    }
+}
+
 int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s) {
     const int64_t S = m_end - m_begin;
     const int64_t d = (int64_t)1 << n;
     if (n < 1 || n > 14) return LRE_EUNSUPPORTED;
     if (S <= 0 || (S & (S - 1)) || m_begin % S || m_end > d) return LRE_EINVAL;
-    static int num_sms = 0;
-    if (!num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    if (use_cl8(layout, n, S)) return launch_cl8_n(n, theta, m_begin, S, mu, s);
     const int Dp = (int)(d + (d >> 4) + 1);
     // shared-memory budget per CTA (masks per CTA = largest power of two that
     // fits): measured best 40 KB at n <= 11 (several CTAs per SM), 75 KB at
@@ -307,7 +565,7 @@ int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64
         if (e != cudaSuccess) return LRE_ECUDA;
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, assemble_pair_kernel<512>, 512, smem);
-        const int64_t grid = 2 * std::min<int64_t>(a.groups, (int64_t)num_sms * std::max(1, per_sm) / 2);
+        const int64_t grid = 2 * std::min<int64_t>(a.groups, (int64_t)num_sms() * std::max(1, per_sm) / 2);
         assemble_pair_kernel<512><<<(unsigned)grid, 512, smem, s>>>(a);
     } else {
         a.cl = 1;
@@ -316,7 +574,7 @@ int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64
         if (e != cudaSuccess) return LRE_ECUDA;
         int per_sm = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, assemble_kernel, threads, smem);
-        const int64_t grid = std::min<int64_t>(a.groups, (int64_t)num_sms * std::max(1, per_sm));
+        const int64_t grid = std::min<int64_t>(a.groups, (int64_t)num_sms() * std::max(1, per_sm));
         assemble_kernel<<<(unsigned)grid, threads, smem, s>>>(a);
     }
     count_launch();

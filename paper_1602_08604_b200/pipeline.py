@@ -55,8 +55,12 @@ def _torch():
 
 
 def _device(device):
+    """A concrete CUDA device (index filled in: torch.device("cuda") != cuda:0 in comparisons)."""
     torch = _torch()
-    return torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.type == "cuda" and dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
 
 
 def _check_kernel(kernel: str) -> None:
@@ -101,8 +105,12 @@ def to_device_record(record_or_source, device=None, stream=None) -> DeviceRecord
             raise ValueError(f"counts shape {counts.shape} != {(3**n, 1 << n)} for n={n}")
         if not np.issubdtype(counts.dtype, np.integer):
             raise ValueError(f"counts must be integers, got dtype {counts.dtype}")
-        if counts.dtype not in (np.uint8, np.uint16, np.int32, np.int64):
-            counts = counts.astype(np.int64)
+        if counts.dtype in (np.uint8, np.uint16) and int(rec.shots) > np.iinfo(counts.dtype).max:
+            # each count fits its dtype but a row sum may not (uint8 with shots > 255):
+            # widen (exactly) to the smallest dtype that holds `shots`, as the kernels need
+            counts = counts.astype(compact_dtype(int(rec.shots)))
+        elif counts.dtype not in (np.uint8, np.uint16, np.int32, np.int64):
+            counts = counts.astype(np.int64)  # int8/int16/uint32/...: exact in int64, validated below
         host = torch.from_numpy(np.ascontiguousarray(counts))
         dcounts = host.to(dev, non_blocking=False)
         drec = DeviceRecord(n=n, shots=int(rec.shots), counts=dcounts, seed=rec.seed, state=rec.state)
@@ -162,12 +170,30 @@ class LREPlan:
         self.theta = torch.empty(4**self.n, dtype=torch.float64, device=self.device)
         self.mu = self.ws[:mu_bytes].view(torch.complex128).view(d, d) if with_mu else None
         self.passes = int(L.lre_step1_num_passes(self.n, self.shots))
+        # theta layout inside the plan: mask-major at n >= 11, where step (ii) is the
+        # 8-CTA-cluster kernel that bulk-copies each mask's 2^n coefficients
+        # (DESIGN.md §4); theta_natural() exports the reference's natural order
+        self.layout = _lib.MASK_MAJOR if self.n >= 11 else _lib.NATURAL
         self._checks = []
 
+    def _check_chunk(self, counts, count_dtype: int, rows: int) -> None:
+        """Shape, dtype, device and contiguity of a counts tensor handed to the C ABI
+        (which sees only a pointer)."""
+        torch = _torch()
+        if not isinstance(counts, torch.Tensor) or not counts.is_cuda or counts.device != self.device:
+            raise ValueError(f"counts must be a CUDA tensor on {self.device}")
+        if counts.dim() != 2 or tuple(counts.shape) != (rows, 1 << self.n):
+            raise ValueError(f"counts shape {tuple(counts.shape)} != {(rows, 1 << self.n)} for n={self.n}")
+        if not counts.is_contiguous():
+            raise ValueError("counts must be contiguous")
+        if lre_dtype_of(counts.dtype) != int(count_dtype):
+            raise ValueError(f"count dtype {counts.dtype} does not match lre dtype code {count_dtype}")
+
     def step1(self, counts, count_dtype: int, stream) -> None:
+        self._check_chunk(counts, count_dtype, 3**self.n)
         _lib.call("lre_step1", counts.data_ptr(), count_dtype, self.n, self.shots, 0, 3**self.n,
                   self.ws.data_ptr(), self.ws_bytes, self.theta.data_ptr(), _lib.OUT_THETA_F64,
-                  _lib.NATURAL, stream.cuda_stream)
+                  self.layout, stream.cuda_stream)
 
     def stage(self, chunk, count_dtype: int, w_begin: int, w_end: int, stream, validate: bool = False) -> None:
         """Fold setting chunk [w_begin, w_end) into the first pass (lre_step1_stage).
@@ -179,6 +205,7 @@ class LREPlan:
         before the reconstruction.  An empty range is a no-op."""
         if int(w_end) == int(w_begin):
             return
+        self._check_chunk(chunk, count_dtype, int(w_end) - int(w_begin))
         if validate:
             torch = _torch()
             res = torch.empty(3, dtype=torch.int64, device=self.device)
@@ -216,12 +243,37 @@ class LREPlan:
 
     def finish(self, stream) -> None:
         _lib.call("lre_step1_finish", self.ws.data_ptr(), self.ws_bytes, self.n, self.shots,
-                  self.theta.data_ptr(), _lib.OUT_THETA_F64, _lib.NATURAL, stream.cuda_stream)
+                  self.theta.data_ptr(), _lib.OUT_THETA_F64, self.layout, stream.cuda_stream)
 
     def step2(self, stream) -> None:
         d = 1 << self.n
-        _lib.call("lre_assemble", self.theta.data_ptr(), _lib.NATURAL, self.n, 0, d, self.mu.data_ptr(),
+        _lib.call("lre_assemble", self.theta.data_ptr(), self.layout, self.n, 0, d, self.mu.data_ptr(),
                   stream.cuda_stream)
+
+    def export_buffer(self):
+        """Room for a natural-order theta copy behind mu in the step-(i) workspace
+        (dead once theta is final; n = 14 has no HBM to spare for a fresh 2 GiB
+        buffer next to a resident record), or None."""
+        if self.layout == _lib.NATURAL:
+            return None
+        torch = _torch()
+        mu_bytes = 0 if self.mu is None else self.mu.numel() * 16
+        off = (mu_bytes + 255) // 256 * 256
+        need = self.theta.numel() * 8
+        if self.ws.numel() < off + need:
+            return None
+        return self.ws[off:off + need].view(torch.float64)
+
+    def theta_natural(self, stream=None, out=None):
+        """theta in the reference's natural order (pipeline.py:138): the plan's own
+        buffer when it is natural, else a relayout (lre_theta_relayout) into `out`."""
+        if self.layout == _lib.NATURAL:
+            return self.theta
+        torch = _torch()
+        stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        out = torch.empty_like(self.theta) if out is None else out
+        _lib.call("lre_theta_relayout", self.theta.data_ptr(), self.layout, self.n, out.data_ptr(), stream.cuda_stream)
+        return out
 
     def run(self, counts, count_dtype: int, stream) -> None:
         self.step1(counts, count_dtype, stream)
@@ -242,7 +294,8 @@ def step_one_least_squares(record_or_source, workers: int = 1, kernel: str = "b2
     stream = torch.cuda.current_stream(rec.counts.device)
     theta = torch.empty(4**n, dtype=torch.float64, device=rec.counts.device)
     if rec.w_begin != 0 or rec.w_end != 3**n:
-        raise ValueError("step_one_least_squares needs the full setting range")
+        raise ValueError(f"step_one_least_squares needs the full setting range [0, {3**n}), "
+                         f"got [{rec.w_begin}, {rec.w_end})")
     import ctypes
 
     ws = ctypes.c_size_t(0)
@@ -269,7 +322,12 @@ def step_two_assemble(theta, workers: int = 1, *, device=None, as_tensor: bool =
     t = t.to(device=dev, dtype=torch.float64).contiguous()
     d = 1 << n
     mu = torch.empty((d, d), dtype=torch.complex128, device=dev)
-    _lib.call("lre_assemble", t.data_ptr(), _lib.NATURAL, n, 0, d, mu.data_ptr(), stream.cuda_stream)
+    layout = _lib.NATURAL
+    if n >= 11:  # the 8-CTA-cluster assembly reads each mask's coefficients contiguously
+        mm = torch.empty_like(t)
+        _lib.call("lre_theta_relayout", t.data_ptr(), _lib.NATURAL, n, mm.data_ptr(), stream.cuda_stream)
+        t, layout = mm, _lib.MASK_MAJOR
+    _lib.call("lre_assemble", t.data_ptr(), layout, n, 0, d, mu.data_ptr(), stream.cuda_stream)
     return mu if as_tensor else mu.cpu().numpy()
 
 
@@ -347,6 +405,8 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
     torch = _torch()
     rec = to_device_record(record_or_source, device)
     n = pauli.check_qubit_count(rec.n)
+    if rec.w_begin != 0 or rec.w_end != 3**n:
+        raise ValueError(f"reconstruct needs the full setting range [0, {3**n}), got [{rec.w_begin}, {rec.w_end})")
     if n > DENSE_PIPELINE_MAX_QUBITS:
         raise ValueError(
             f"n={n} needs a dense {2**n}x{2**n} complex allocation "
@@ -355,18 +415,27 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
     dev = rec.counts.device
     stream = torch.cuda.current_stream(dev)
     plan = LREPlan(n, rec.shots, dev)
+    nvtx = torch.cuda.nvtx
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     ev[0].record(stream)
+    nvtx.range_push("lre.step1")
     plan.step1(rec.counts, rec.lre_dtype, stream)
+    nvtx.range_pop()
     ev[1].record(stream)
+    nvtx.range_push("lre.step2")
     plan.step2(stream)
+    nvtx.range_pop()
     ev[2].record(stream)
+    nvtx.range_push("lre.step3")
     if project:
         rho, evals = step_three_project(plan.mu)
     else:
         rho, evals = plan.mu, None
+    nvtx.range_pop()
     ev[3].record(stream)
-    theta = plan.theta
+    nvtx.range_push("lre.theta_export")
+    theta = plan.theta_natural(stream, out=plan.export_buffer())
+    nvtx.range_pop()
     ev[4].record(stream)
     ev[4].synchronize()
     t1 = ev[0].elapsed_time(ev[1]) / 1e3
@@ -380,7 +449,9 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
         "threads": workers,
         "kernel": kernel,
         "gpus": 1,
+        "t_theta_export_s": ev[3].elapsed_time(ev[4]) / 1e3,
     }
+    timings.update(roofline_timings(n, rec.counts.element_size(), t1 + t2))
     mu = plan.mu
     if not as_tensor:
         same = rho is mu
@@ -388,6 +459,33 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
         rho = mu if same else rho.cpu().numpy()
         evals = None if evals is None else evals.cpu().numpy()
     return ReconstructionResult(theta=theta, mu=mu, rho=rho, eigenvalues=evals, timings=timings)
+
+
+def hbm_peak_gbps() -> tuple[float, str]:
+    """Roofline denominator: the measured copy bandwidth of this pool's B200s
+    (MEASURED_PEAKS.json, driver-written), else the profiling guide's fallback."""
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes(n: int, count_bytes: int) -> float:
+    """B(n) = c 6^n (counts read once) + 32 4^n (theta written and read, mu written)."""
+    return count_bytes * 6.0**n + 32.0 * 4.0**n
+
+
+def roofline_timings(n: int, count_bytes: int, seconds: float) -> dict:
+    """SURVEY §5 instrumentation keys: algorithmic bytes of steps (i)+(ii), achieved GB/s, fraction of peak."""
+    b = algorithmic_bytes(n, count_bytes)
+    peak, kind = hbm_peak_gbps()
+    gbps = b / seconds / 1e9 if seconds > 0 else float("nan")
+    return {"bytes": b, "gbps": gbps, "roofline_frac": gbps / peak, "peak_gbps": peak, "peak_kind": kind}
 
 
 def reconstruct_generated(state: StateDescriptor, shots: int, seed: int, *, device=None, project: bool = True,
@@ -428,7 +526,7 @@ def reconstruct_generated(state: StateDescriptor, shots: int, seed: int, *, devi
     t1, t2, t3 = (ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(3))
     timings = {"t_generate_and_step1_s": t1, "t_step2_s": t2, "t_step3_s": t3, "t_total_s": t1 + t2 + t3,
                "threads": 1, "kernel": "b200", "gpus": 1}
-    theta, mu = plan.theta, plan.mu
+    theta, mu = plan.theta_natural(stream, out=plan.export_buffer()), plan.mu
     if not as_tensor:
         same = rho is mu
         theta, mu = theta.cpu().numpy(), mu.cpu().numpy()

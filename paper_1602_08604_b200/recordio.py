@@ -306,7 +306,7 @@ def reconstruct_file(path_or_file, *, device=None, project: bool = False, chunk_
     t1, t2, t3 = (ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(3))
     timings = {"t_ingest_s": t_ingest, "t_step1_s": t1, "t_step2_s": t2, "t_step3_s": t3,
                "t_total_s": t_ingest + t1 + t2 + t3, "threads": 1, "kernel": "b200", "gpus": 1}
-    theta, mu = plan.theta, plan.mu
+    theta, mu = plan.theta_natural(comp, out=plan.export_buffer()), plan.mu
     if not as_tensor:
         same = rho is mu
         theta, mu = theta.cpu().numpy(), mu.cpu().numpy()
