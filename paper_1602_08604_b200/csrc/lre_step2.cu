@@ -266,41 +266,85 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT, 1) assemble_pair
 }
 
 // ---------------------------------------------------------------------------
-// n >= 11, mask-major theta: assemble_cl8_kernel<LOGD>
+// n >= 11, mask-major theta: assemble_x8_kernel<LOGD>
 //
 // The write pattern decides this kernel (profiles/r02_microbench_mu_writes.txt,
 // 4.3 GB of XOR-diagonal stores at n = 14): a row segment of 16 B (one mask)
-// runs at 1.1 TB/s, 32 B (a mask pair) at 2.9-3.6 TB/s and 64 B at 2.9-4.7
-// TB/s depending on whether the CTAs writing the two halves of a 128-byte line
-// happen to be in step; only whole 128-byte lines (8 consecutive masks per
-// row) hold 4.6 TB/s for any schedule.  One mask's transform is 2^n doubles
-// (128 KB at n = 14), so 8 masks cannot share one SM:
-//   * a cluster of 8 CTAs owns an aligned block of 8 masks, CTA j the
-//     transform of mask m0 + j, in its own shared memory;
-//   * theta arrives mask-major (each mask's 2^n coefficients contiguous) by
-//     bulk copies (cp.async.bulk, mbarrier completion): the first half of the
-//     next mask is prefetched into a staging buffer while the current mask is
-//     written out, the second half lands in the transform buffer as soon as
-//     the partners have finished reading it;
-//   * the fp64 WHT runs in three shared-memory rounds (bits 5-9 with the sign
-//     twist, bits 0-4, bits 10..n-1), one pad double per 32 (conflict-free);
-//   * after one cluster barrier CTA c writes rows [c d/8, (c+1) d/8): per row
-//     16 transform values (two per mask, 14 of them read from the partners
-//     through distributed shared memory) -> one 128-byte segment.
+// runs at 0.4-1.1 TB/s, 32 B (a mask pair) at 1.4-3.6 TB/s and 64 B at
+// 2.4-4.7 TB/s depending on when the other parts of each 128-byte line are
+// written (partial lines evicted early are read-modify-written); only whole
+// 128-byte lines (8 consecutive masks per row, written by one thread) hold
+// 4.5-4.7 TB/s for any schedule.  One mask's transform is 2^n doubles (128 KB
+// at n = 14), so the 8 masks of a line live on the 8 CTAs of a cluster.
+//
+// SPLIT mode (all but ~3% of the mask blocks): the block's masks m0..m0+7
+// share three zero bits b0 < b1 < b2 in [3, n).  Every row r and its partner
+// r ^ m then agree on those bits, so the transform splits exactly into eighths:
+// for r with (r_b0, r_b1, r_b2) = k,
+//     F_m[r] = WHT_{n-3}( G_{m,k} )[r'],   G_{m,k}[a'] = sum_s (-1)^{s.k} w_m[a' with s inserted],
+// (r', a' = the index with the three bits removed).  CTA j loads its own mask
+// m0 + j (contiguous, mask-major theta) straight into registers, applies the
+// sign twist and the 3-bit butterfly, and pushes eighth k to CTA k with
+// st.async (distributed shared memory, completing on CTA k's mbarrier).  CTA
+// k then holds eighth k of all 8 masks (2^n doubles), transforms them locally
+// and writes its 2^(n-3) rows as whole 128-byte lines, reading only its own
+// shared memory.  One relaxed cluster barrier per block protects the buffers;
+// no release fence waits on the streaming mu stores, and the next block's
+// theta loads are in flight (registers) during the write phase.
+// FULL mode (blocks with fewer than three common zero bits): CTA j bulk-copies
+// its mask, transforms all 2^n coefficients, and the write phase pulls the
+// partners' values through distributed shared memory.
 // ---------------------------------------------------------------------------
-template <int LOGD> struct Cl8 {
+template <int LOGD> struct X8 {
     static constexpr int D = 1 << LOGD;
-    static constexpr int NT = D / 32;     // threads per CTA
-    static constexpr int FP = D + D / 32; // padded transform (doubles)
-    static constexpr int HALF = D / 2;    // prefetched first half (doubles)
-    static constexpr int FH = HALF + HALF / 32;  // linear landing offset of the second half inside F
-    static constexpr size_t SMEM = (size_t)(FP + HALF) * sizeof(double) + 2 * sizeof(uint64_t);
-    static constexpr uint32_t HALF_BYTES = (uint32_t)HALF * sizeof(double);
+    static constexpr int NT = D / 32;                  // threads per CTA
+    static constexpr int L = LOGD - 3;                 // bits of an eighth
+    static constexpr int E = 1 << L;                   // eighth length
+    static constexpr int EP = E + E / 16 + 2;          // padded eighth stride (2 per 32; even; shifts banks per mask)
+    static constexpr int FULLP = D + D / 32;           // FULL mode: one pad double per 32
+    static constexpr int FD = 8 * EP > FULLP ? 8 * EP : FULLP;
+    static constexpr size_t STAGE = (size_t)8 * NT * 16;  // next block's second a' pair (cp.async)
+    static constexpr size_t SMEM = (size_t)FD * sizeof(double) + STAGE + 16;
 };
 
 __device__ __forceinline__ int pad32(int x) { return x + (x >> 5); }
+__device__ __forceinline__ int pad2_32(int x) { return x + 2 * (x >> 5); }
 
-struct Cl8Args {
+// insert bit values (s0, s1, s2) at final positions b0 < b1 < b2
+__device__ __forceinline__ uint32_t ins3(uint32_t x, int b0, int b1, int b2, uint32_t s) {
+    x = ((x >> b0) << (b0 + 1)) | ((s & 1u) << b0) | (x & ((1u << b0) - 1));
+    x = ((x >> b1) << (b1 + 1)) | (((s >> 1) & 1u) << b1) | (x & ((1u << b1) - 1));
+    x = ((x >> b2) << (b2 + 1)) | (((s >> 2) & 1u) << b2) | (x & ((1u << b2) - 1));
+    return x;
+}
+__device__ __forceinline__ uint32_t del3(uint32_t x, int b0, int b1, int b2) {
+    x = ((x >> (b2 + 1)) << b2) | (x & ((1u << b2) - 1));
+    x = ((x >> (b1 + 1)) << b1) | (x & ((1u << b1) - 1));
+    x = ((x >> (b0 + 1)) << b0) | (x & ((1u << b0) - 1));
+    return x;
+}
+
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, int rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_v2(uint32_t raddr, double x, double y, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+                 "d"(x), "d"(y), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ double2 ld_nc_v2(const double *p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
+struct X8Args {
     const double *theta;  // mask-major slice: theta[(m - m_begin) * 2^n + a]
     int64_t m_begin;
     int64_t S;            // masks in the slice (power of two >= 8); mu rows are S complex wide
@@ -309,177 +353,351 @@ struct Cl8Args {
     double2 *mu;
 };
 
+// three highest zero bits of m0 in [3, n) (b0 < b1 < b2); false if fewer than three
+__device__ __forceinline__ bool split_bits(uint32_t m0, int n, int &b0, int &b1, int &b2) {
+    uint32_t z = ~m0 & (((1u << n) - 1) & ~7u);
+    if (__popc(z) < 3) return false;
+    b2 = 31 - __clz(z);
+    z &= ~(1u << b2);
+    b1 = 31 - __clz(z);
+    z &= ~(1u << b1);
+    b0 = 31 - __clz(z);
+    return true;
+}
+
+// the 8 double2 theta loads of one thread's a' pair q for SPLIT block u (8 split combinations)
 template <int LOGD>
-__device__ __forceinline__ void cl8_issue_half(const Cl8Args &a, int64_t u, int rank, int half, double *dst,
-                                               uint64_t *bar) {
-    using C = Cl8<LOGD>;
-    const double *src = a.theta + ((u * 8 + rank) << LOGD) + (int64_t)half * C::HALF;
-    constexpr uint32_t CHUNK = C::HALF_BYTES < 16384u ? C::HALF_BYTES : 16384u;
-    mbar_expect_tx(bar, C::HALF_BYTES);
-#pragma unroll 1
-    for (uint32_t off = 0; off < C::HALF_BYTES; off += CHUNK)
-        bulk_load(reinterpret_cast<char *>(dst) + off, reinterpret_cast<const char *>(src) + off, CHUNK, bar);
+__device__ __forceinline__ void x8_load(const X8Args &a, int64_t u, int rank, int t, int q, int b0, int b1, int b2,
+                                        double2 (&v)[8]) {
+    using C = X8<LOGD>;
+    const double *src = a.theta + ((u * 8 + rank) << LOGD) + ins3(2u * (uint32_t)(t + C::NT * q), b0, b1, b2, 0u);
+    const uint32_t P0 = 1u << b0, P1 = 1u << b1, P2 = 1u << b2;
+#pragma unroll
+    for (int sc = 0; sc < 8; ++sc)
+        v[sc] = ld_nc_v2(src + ((sc & 1 ? P0 : 0u) | (sc & 2 ? P1 : 0u) | (sc & 4 ? P2 : 0u)));
+}
+
+// the same 8 pairs as x8_load, copied asynchronously into this thread's stage slots
+template <int LOGD>
+__device__ __forceinline__ void x8_stage(const X8Args &a, int64_t u, int rank, int t, int q, int b0, int b1, int b2,
+                                         double2 *stg) {
+    using C = X8<LOGD>;
+    const double *src = a.theta + ((u * 8 + rank) << LOGD) + ins3(2u * (uint32_t)(t + C::NT * q), b0, b1, b2, 0u);
+    const uint32_t P0 = 1u << b0, P1 = 1u << b1, P2 = 1u << b2;
+#pragma unroll
+    for (int sc = 0; sc < 8; ++sc)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(stg + sc * C::NT)),
+                     "l"(src + ((sc & 1 ? P0 : 0u) | (sc & 2 ? P1 : 0u) | (sc & 4 ? P2 : 0u)))
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 template <int LOGD>
-__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(Cl8<LOGD>::NT, LOGD >= 14 ? 1 : LOGD == 13 ? 2 : 4) assemble_cl8_kernel(const Cl8Args a) {
-    using C = Cl8<LOGD>;
-    constexpr int D = C::D, NT = C::NT;
-    extern __shared__ __align__(16) double cl8_smem[];
-    double *F = cl8_smem;
-    double *Sbuf = cl8_smem + C::FP;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(Sbuf + C::HALF);
-    uint64_t *barS = bars, *barF = bars + 1;
+__global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >= 14 ? 1 : LOGD == 13 ? 2 : 4)
+    assemble_x8_kernel(const X8Args a) {
+    using C = X8<LOGD>;
+    constexpr int D = C::D, NT = C::NT, E = C::E, EP = C::EP;
+    extern __shared__ __align__(16) double x8_smem[];
+    double *F = x8_smem;
+    uint64_t *barR = reinterpret_cast<uint64_t *>(reinterpret_cast<char *>(x8_smem + C::FD) + C::STAGE);
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
     const int t = threadIdx.x;
     const int64_t ncl = gridDim.x / 8;
-    const int64_t u0 = blockIdx.x / 8;
+    const uint32_t F_s = smem_u32(F), bar_s = smem_u32(barR);
+
     if (t == 0) {
-        mbar_init(barS, 1);
-        mbar_init(barF, 1);
+        mbar_init(barR, 1);
         fence_mbar_init();
-        if (u0 < a.units) {
-            cl8_issue_half<LOGD>(a, u0, rank, 0, Sbuf, barS);
-            cl8_issue_half<LOGD>(a, u0, rank, 1, F + C::FH, barF);
+    }
+    cluster.sync();  // every CTA's mbarrier is initialised before any remote st.async
+
+    int64_t u = blockIdx.x / 8;
+    // the next block's a' pairs are in flight during the write phase: pair 0 in
+    // registers, pair 1 in a per-thread shared-memory stage (cp.async, [combination][thread])
+    double2 v[8];
+    double2 *stg = reinterpret_cast<double2 *>(x8_smem + C::FD) + t;
+    int b0 = 0, b1 = 0, b2 = 0;
+    bool split = false;
+    if (u < a.units) {
+        split = split_bits((uint32_t)(a.m_begin + u * 8), LOGD, b0, b1, b2);
+        if (split) {
+            x8_load<LOGD>(a, u, rank, t, 0, b0, b1, b2, v);
+            x8_stage<LOGD>(a, u, rank, t, 1, b0, b1, b2, stg);
         }
     }
-    __syncthreads();
     uint32_t parity = 0;
-    for (int64_t u = u0; u < a.units; u += ncl, parity ^= 1) {
-        const uint32_t m = (uint32_t)(a.m_begin + u * 8 + rank);  // this CTA's mask
-        // ---- round A: bits 5..9 (+ sign twist), read linear, write padded ----
-        {
-            const int g = t >> 5, l = t & 31;
-            const int base = g * 1024 + l;
-            const double *src = base < C::HALF ? Sbuf + base : F + C::FH + (base - C::HALF);
-            double v[32];
-            mbar_wait(base < C::HALF ? barS : barF, parity);
+    bool first = true;
+    for (; u < a.units; u += ncl, parity ^= 1) {
+        const uint32_t m0 = (uint32_t)(a.m_begin + u * 8);
+        const int64_t smask = a.S - 1;
+        if (!first) cluster_wait();  // every CTA has finished reading its buffer for the previous block
+        first = false;
+        if (split) {
+            // ---- push: twist + 3-bit butterfly of this CTA's mask, eighth k -> CTA k ----
+            if (t == 0) mbar_expect_tx(barR, (uint32_t)D * sizeof(double));
+            const uint32_t mj = m0 + (uint32_t)rank;
+            double2 v1[8];
+            asm volatile("cp.async.wait_all;" ::: "memory");
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint32_t av = (uint32_t)(base + 32 * j);
-                const double x = src[32 * j];
-                v[j] = ((__popc(av & m) >> 1) & 1) ? -x : x;
+            for (int sc = 0; sc < 8; ++sc) v1[sc] = stg[sc * NT];
+            // g[q][e][k]: a' = ap_q + e (ap_q = 2 (t + NT q): q selects the top bit L-1 of a', e bit 0)
+            double g[2][2][8];
+#pragma unroll
+            for (int sc = 0; sc < 8; ++sc) {
+                g[0][0][sc] = v[sc].x;
+                g[0][1][sc] = v[sc].y;
+                g[1][0][sc] = v1[sc].x;
+                g[1][1][sc] = v1[sc].y;
             }
+            // 3-bit butterfly over the split bits (sc -> eighth k)
 #pragma unroll
-            for (int h = 1; h < 32; h <<= 1)
+            for (int h = 1; h < 8; h <<= 1)
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (!(j & h)) {
-                        const double x = v[j], y = v[j + h];
-                        v[j] = x + y;
-                        v[j + h] = x - y;
-                    }
-            __syncthreads();  // every read of the second half (landed inside F) precedes the padded writes
+                for (int sc = 0; sc < 8; ++sc)
+                    if (!(sc & h)) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) F[pad32(base + 32 * j)] = v[j];
-        }
-        __syncthreads();
-        // the staging buffer is consumed: prefetch the first half of the next mask
-        if (t == 0 && u + ncl < a.units) {
-            fence_proxy_async_smem();
-            cl8_issue_half<LOGD>(a, u + ncl, rank, 0, Sbuf, barS);
-        }
-        // ---- round B: bits 0..4 (32 consecutive elements per thread) ----
-        {
-            double *b = F + 33 * t;
-            double v[32];
+                        for (int q = 0; q < 2; ++q)
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = b[i];
-#pragma unroll
-            for (int h = 1; h < 32; h <<= 1)
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (!(i & h)) {
-                        const double x = v[i], y = v[i + h];
-                        v[i] = x + y;
-                        v[i + h] = x - y;
-                    }
-#pragma unroll
-            for (int i = 0; i < 32; ++i) b[i] = v[i];
-        }
-        __syncthreads();
-        // ---- round C: bits 10..LOGD-1 ----
-        if constexpr (LOGD > 10) {
-            constexpr int K = 1 << (LOGD - 10);
-#pragma unroll 1
-            for (int bse = t; bse < 1024; bse += NT) {
-                double v[K];
-#pragma unroll
-                for (int j = 0; j < K; ++j) v[j] = F[pad32(bse + 1024 * j)];
-#pragma unroll
-                for (int h = 1; h < K; h <<= 1)
-#pragma unroll
-                    for (int j = 0; j < K; ++j)
-                        if (!(j & h)) {
-                            const double x = v[j], y = v[j + h];
-                            v[j] = x + y;
-                            v[j + h] = x - y;
-                        }
-#pragma unroll
-                for (int j = 0; j < K; ++j) F[pad32(bse + 1024 * j)] = v[j];
-            }
-        }
-        // ---- all 8 transforms of the cluster complete and visible ----
-        cluster.sync();
-        // ---- write phase: rows [rank d/8, (rank+1) d/8), one 128-byte segment each ----
-        {
-            const uint32_t m0 = (uint32_t)(a.m_begin + u * 8);
-            const int64_t smask = a.S - 1;
-#pragma unroll 1
-            for (int k = 0; k < 4; k += 2) {
-                // loads: mask j uniform across the warp, lanes on consecutive rows -> each
-                // warp access reads one partner's shared memory contiguously
-                double2 o[2][8];  // [row][mask j]: mu[r, r ^ (m0 + j)]
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const double *Fj = cluster.map_shared_rank(F, j);
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const int r = rank * (D / 8) + t + NT * (k + q);
-                        const double f1 = Fj[pad32(r)], f2 = Fj[pad32(r ^ (int)(m0 + j))];
-                        o[q][j] = make_double2(a.scale_half * (f1 + f2), a.scale_half * (f2 - f1));
-                    }
-                }
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int r = rank * (D / 8) + t + NT * (k + q);
-                    // column slot of mask j is (r & 7) ^ j: permute the register array by
-                    // XOR with r & 7 (three conditional swap stages)
-#pragma unroll
-                    for (int b = 0; b < 3; ++b) {
-                        const bool sw = (r >> b) & 1;
-#pragma unroll
-                        for (int x = 0; x < 8; ++x)
-                            if (!(x & (1 << b))) {
-                                const double2 lo = o[q][x], hi = o[q][x | (1 << b)];
-                                o[q][x] = sw ? hi : lo;
-                                o[q][x | (1 << b)] = sw ? lo : hi;
+                            for (int e = 0; e < 2; ++e) {
+                                const double x = g[q][e][sc], y = g[q][e][sc + h];
+                                g[q][e][sc] = x + y;
+                                g[q][e][sc + h] = x - y;
                             }
                     }
-                    const int64_t cb = (int64_t)((uint32_t)r ^ m0) & smask & ~(int64_t)7;
-                    double2 *dst = a.mu + (int64_t)r * a.S + cb;
+            // sign twist (-1)^floor(pc(a & m)/2): the split bits are zero in m, so it is one
+            // sign per a' for all eight combinations (applied after the linear butterfly)
 #pragma unroll
-                    for (int w = 0; w < 4; ++w) st256_cs(dst + 2 * w, o[q][2 * w], o[q][2 * w + 1]);
+            for (int q = 0; q < 2; ++q) {
+                const int pc = __popc(ins3(2u * (uint32_t)(t + NT * q), b0, b1, b2, 0u) & mj);
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const uint64_t neg = (uint64_t)(((pc + (e ? (int)(mj & 1u) : 0)) >> 1) & 1) << 63;
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        g[q][e][k] = __longlong_as_double(__double_as_longlong(g[q][e][k]) ^ (long long)neg);
+                }
+            }
+            // the WHT stages of a' bits 0 (e) and L-1 (q) are in registers already
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double x = g[q][0][k], y = g[q][1][k];
+                    g[q][0][k] = x + y;
+                    g[q][1][k] = x - y;
+                }
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double x = g[0][e][k], y = g[1][e][k];
+                    g[0][e][k] = x + y;
+                    g[1][e][k] = x - y;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const uint32_t off = (uint32_t)(rank * EP + pad2_32(2 * (t + NT * q))) * sizeof(double);
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    st_async_v2(mapa_u32(F_s + off, k), g[q][0][k], g[q][1][k], mapa_u32(bar_s, k));
+            }
+            mbar_wait(barR, parity);
+            // ---- WHT over a' bits 1 .. L-2 of the 8 eighths (this CTA's k = rank) ----
+            {  // bits 1..4: 32 consecutive elements per thread (16-byte accesses, conflict-free)
+                const int arr = t / (E / 32), blk = t % (E / 32);
+                double2 *b = reinterpret_cast<double2 *>(F + arr * EP + 34 * blk);
+                double w[32];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const double2 x = b[i];
+                    w[2 * i] = x.x;
+                    w[2 * i + 1] = x.y;
+                }
+#pragma unroll
+                for (int h = 2; h < 32; h <<= 1)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (!(i & h)) {
+                            const double x = w[i], y = w[i + h];
+                            w[i] = x + y;
+                            w[i + h] = x - y;
+                        }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) b[i] = make_double2(w[2 * i], w[2 * i + 1]);
+            }
+            __syncthreads();
+            {  // bits 5 .. L-2 (hi = bit L-1 was done by the producers)
+                constexpr int K = 1 << (C::L - 6);
+                constexpr int ITEMS = 8 * E / K;
+#pragma unroll 1
+                for (int it = t; it < ITEMS; it += NT) {
+                    const int arr = it / (E / K), rest = it % (E / K);
+                    const int lo = rest & 31, hi = rest >> 5;
+                    double *b = F + arr * EP + lo + 34 * K * hi;
+                    double w[K];
+#pragma unroll
+                    for (int i = 0; i < K; ++i) w[i] = b[34 * i];
+#pragma unroll
+                    for (int h = 1; h < K; h <<= 1)
+#pragma unroll
+                        for (int i = 0; i < K; ++i)
+                            if (!(i & h)) {
+                                const double x = w[i], y = w[i + h];
+                                w[i] = x + y;
+                                w[i + h] = x - y;
+                            }
+#pragma unroll
+                    for (int i = 0; i < K; ++i) b[34 * i] = w[i];
+                }
+            }
+            __syncthreads();
+            // ---- next block's theta into registers (in flight during the write phase) ----
+            const int cb0 = b0, cb1 = b1, cb2 = b2;
+            const int64_t un = u + ncl;
+            bool nsplit = false;
+            if (un < a.units) {
+                nsplit = split_bits((uint32_t)(a.m_begin + un * 8), LOGD, b0, b1, b2);
+                if (nsplit) {
+                    x8_load<LOGD>(a, un, rank, t, 0, b0, b1, b2, v);
+                    x8_stage<LOGD>(a, un, rank, t, 1, b0, b1, b2, stg);
+                }
+            }
+            // ---- write phase: rows with split bits = rank, whole 128-byte lines ----
+            const uint32_t m0c = del3(m0, cb0, cb1, cb2);
+            const uint32_t rpat = ins3(0u, cb0, cb1, cb2, (uint32_t)rank);
+            // a warp writes 8 rows per step, 4 lanes per row: lane (rr, w) stores the
+            // 32-byte slot pair w of row rr, so every store instruction covers 8 whole
+            // 128-byte lines (the L1 processes 8 lines, not 32 partial ones)
+            const int lane = t & 31, warp = t >> 5;
+            const int rr = lane >> 2, w = lane & 3;
+            const int j0 = rr ^ (2 * w), j1 = j0 ^ 1;  // masks of slots 2w, 2w+1 (row & 7 == rr)
+            const double *A0 = F + j0 * EP, *A1 = F + j1 * EP;  // slot s of row r holds mask (r & 7) ^ s
+#pragma unroll 4
+            for (int g8 = warp; g8 < E / 8; g8 += NT / 32) {
+                const int rp = 8 * g8 + rr;
+                const uint32_t r = ins3((uint32_t)rp, cb0, cb1, cb2, 0u) | rpat;
+                const double f1a = A0[pad2_32(rp)], f2a = A0[pad2_32(rp ^ (int)(m0c + j0))];
+                const double f1b = A1[pad2_32(rp)], f2b = A1[pad2_32(rp ^ (int)(m0c + j1))];
+                const double2 oa = make_double2(a.scale_half * (f1a + f2a), a.scale_half * (f2a - f1a));
+                const double2 ob = make_double2(a.scale_half * (f1b + f2b), a.scale_half * (f2b - f1b));
+                double2 *dst = a.mu + (int64_t)r * a.S + ((int64_t)(r ^ m0) & smask & ~(int64_t)7) + 2 * w;
+                st256_cs(dst, oa, ob);
+            }
+            split = nsplit;
+        } else {
+            // ---- FULL mode: this CTA transforms its whole mask; partners pull ----
+            if (t == 0) {
+                fence_proxy_async_smem();
+                mbar_expect_tx(barR, (uint32_t)D * sizeof(double));
+                const double *src = a.theta + ((u * 8 + rank) << LOGD);
+                constexpr uint32_t CH = 16384;
+#pragma unroll 1
+                for (uint32_t off = 0; off < (uint32_t)D * sizeof(double); off += CH)
+                    bulk_load(reinterpret_cast<char *>(F) + off, reinterpret_cast<const char *>(src) + off, CH, barR);
+            }
+            mbar_wait(barR, parity);
+            const uint32_t m = m0 + (uint32_t)rank;
+            {  // bits 5..9 with the sign twist; read all (linear), then write padded
+                const int g = t >> 5, l = t & 31;  // NT = D / 32 threads = one (group, lane) each
+                const int base = g * 1024 + l;
+                double w[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t av = (uint32_t)(base + 32 * j);
+                    const double x = F[base + 32 * j];
+                    w[j] = ((__popc(av & m) >> 1) & 1) ? -x : x;
+                }
+#pragma unroll
+                for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (!(j & h)) {
+                            const double x = w[j], y = w[j + h];
+                            w[j] = x + y;
+                            w[j + h] = x - y;
+                        }
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) F[pad32(base + 32 * j)] = w[j];
+            }
+            __syncthreads();
+            {  // bits 0..4
+                double *b = F + 33 * t;
+                double w[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) w[i] = b[i];
+#pragma unroll
+                for (int h = 1; h < 32; h <<= 1)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (!(i & h)) {
+                            const double x = w[i], y = w[i + h];
+                            w[i] = x + y;
+                            w[i + h] = x - y;
+                        }
+#pragma unroll
+                for (int i = 0; i < 32; ++i) b[i] = w[i];
+            }
+            if constexpr (LOGD > 10) {  // bits 10..n-1
+                __syncthreads();
+                constexpr int K = 1 << (LOGD - 10);
+#pragma unroll 1
+                for (int bse = t; bse < 1024; bse += NT) {
+                    double w[K];
+#pragma unroll
+                    for (int j = 0; j < K; ++j) w[j] = F[pad32(bse + 1024 * j)];
+#pragma unroll
+                    for (int h = 1; h < K; h <<= 1)
+#pragma unroll
+                        for (int j = 0; j < K; ++j)
+                            if (!(j & h)) {
+                                const double x = w[j], y = w[j + h];
+                                w[j] = x + y;
+                                w[j + h] = x - y;
+                            }
+#pragma unroll
+                    for (int j = 0; j < K; ++j) F[pad32(bse + 1024 * j)] = w[j];
+                }
+            }
+            cluster.sync();  // the 8 transforms are complete and visible to the partners
+            // rows [rank d/8, (rank+1) d/8): partners' values through distributed shared memory
+#pragma unroll 1
+            for (int q = 0; q < 4; ++q) {
+                const int r = rank * (D / 8) + t + NT * q;
+                double2 *dst = a.mu + (int64_t)r * a.S + ((int64_t)((uint32_t)r ^ m0) & smask & ~(int64_t)7);
+                const int rho = r & 7;
+#pragma unroll
+                for (int J = 0; J < 4; ++J) {
+                    const double *A0 = cluster.map_shared_rank(F, 2 * J), *A1 = cluster.map_shared_rank(F, 2 * J + 1);
+                    const double f1a = A0[pad32(r)], f2a = A0[pad32(r ^ (int)(m0 + 2 * J))];
+                    const double f1b = A1[pad32(r)], f2b = A1[pad32(r ^ (int)(m0 + 2 * J + 1))];
+                    const double2 oa = make_double2(a.scale_half * (f1a + f2a), a.scale_half * (f2a - f1a));
+                    const double2 ob = make_double2(a.scale_half * (f1b + f2b), a.scale_half * (f2b - f1b));
+                    const bool sw = rho & 1;
+                    st256_cs(dst + 2 * ((rho >> 1) ^ J), sw ? ob : oa, sw ? oa : ob);
+                }
+            }
+            const int64_t un = u + ncl;
+            if (un < a.units) {
+                split = split_bits((uint32_t)(a.m_begin + un * 8), LOGD, b0, b1, b2);
+                if (split) {
+                    x8_load<LOGD>(a, un, rank, t, 0, b0, b1, b2, v);
+                    x8_stage<LOGD>(a, un, rank, t, 1, b0, b1, b2, stg);
                 }
             }
         }
-        // partners have finished reading this CTA's transform (their loads were consumed by stores)
-        cluster_sync_relaxed();
-        if (t == 0 && u + ncl < a.units) {
-            fence_proxy_async_smem();
-            cl8_issue_half<LOGD>(a, u + ncl, rank, 1, F + C::FH, barF);
-        }
+        cluster_arrive_relaxed();  // this CTA is done reading its own buffer (and, FULL mode, the partners')
     }
+    if (!first) cluster_wait();  // partners may still read this CTA's shared memory (FULL mode)
 }
 
 template <int LOGD>
-static int launch_cl8(const double *theta, int64_t m_begin, int64_t S, double *mu, cudaStream_t s) {
-    using C = Cl8<LOGD>;
-    auto kern = assemble_cl8_kernel<LOGD>;
+static int launch_x8(const double *theta, int64_t m_begin, int64_t S, double *mu, cudaStream_t s) {
+    using C = X8<LOGD>;
+    auto kern = assemble_x8_kernel<LOGD>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
         return LRE_ECUDA;
-    Cl8Args a;
+    X8Args a;
     a.theta = theta;
     a.m_begin = m_begin;
     a.S = S;
@@ -507,8 +725,8 @@ static int launch_cl8(const double *theta, int64_t m_begin, int64_t S, double *m
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
 }
 
-// the cluster kernel applies to mask-major slices of >= 8 masks at n >= 11 (one
-// round-A group of 1024 coefficients must lie inside one half of a mask)
+// the cluster kernel applies to mask-major slices of >= 8 masks at n >= 11
+// (LRE_ASM=legacy selects the round-1 kernels for A/B runs)
 // (LRE_ASM=legacy selects the round-1 kernels for A/B runs)
 static bool use_cl8(int layout, int n, int64_t S) {
     static const bool legacy = [] {
@@ -520,10 +738,10 @@ static bool use_cl8(int layout, int n, int64_t S) {
 
 static int launch_cl8_n(int n, const double *theta, int64_t m_begin, int64_t S, double *mu, cudaStream_t s) {
     switch (n) {
-    case 11: return launch_cl8<11>(theta, m_begin, S, mu, s);
-    case 12: return launch_cl8<12>(theta, m_begin, S, mu, s);
-    case 13: return launch_cl8<13>(theta, m_begin, S, mu, s);
-    case 14: return launch_cl8<14>(theta, m_begin, S, mu, s);
+    case 11: return launch_x8<11>(theta, m_begin, S, mu, s);
+    case 12: return launch_x8<12>(theta, m_begin, S, mu, s);
+    case 13: return launch_x8<13>(theta, m_begin, S, mu, s);
+    case 14: return launch_x8<14>(theta, m_begin, S, mu, s);
     default: return LRE_EUNSUPPORTED;
     }
 }

@@ -41,6 +41,55 @@ __global__ void __launch_bounds__(512) xor_write(double2 *mu, int logd) {
   }
 }
 
+// Grouped: a CTA (or a CTA pair for SPLIT = 2) writes the G consecutive units of one
+// 128-byte line group back to back, rows rotated per group (groups desynchronised).
+template <int SEG, int SPLIT, int G>
+__global__ void __launch_bounds__(512) xor_write_grouped(double2 *mu, int logd) {
+  const int64_t d = (int64_t)1 << logd;
+  const int64_t groups = d / (SEG * G);
+  const int part = blockIdx.x % SPLIT;
+  const int64_t slots = gridDim.x / SPLIT;
+  for (int64_t g = blockIdx.x / SPLIT; g < groups; g += slots) {
+    const int64_t rows = d / SPLIT;
+    const int64_t rot = (g * 1536) % rows;
+    for (int k = 0; k < G; ++k) {
+      const int64_t m0 = (g * G + k) * SEG;
+      for (int64_t i0 = threadIdx.x; i0 < rows; i0 += blockDim.x) {
+        const int64_t i = (i0 + rot) & (rows - 1);
+        const int64_t r = part * rows + i;
+        const int64_t c0 = (r ^ m0) & ~(int64_t)(SEG - 1);
+        double2 *dst = mu + r * d + c0;
+        const double v = (double)(r + m0);
+        if constexpr (SEG == 1) {
+          __stcs(dst, make_double2(v, -v));
+        } else {
+#pragma unroll
+          for (int q = 0; q < SEG / 2; ++q) st256(dst + 2 * q, v, -v, v + 1, -v - 1);
+        }
+      }
+    }
+  }
+}
+
+template <int SEG, int SPLIT, int G>
+int rung(double2 *mu, int logd, int bpsm, const char *name) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int grid = 148 * bpsm;
+  xor_write_grouped<SEG, SPLIT, G><<<grid, 512>>>(mu, logd);
+  CK(cudaDeviceSynchronize());
+  cudaEventRecord(e0);
+  for (int i = 0; i < 3; ++i) xor_write_grouped<SEG, SPLIT, G><<<grid, 512>>>(mu, logd);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double bytes = 16.0 * (double)(1LL << (2 * logd));
+  printf("%-34s bpsm=%d  %.3f ms  %.1f GB/s\n", name, bpsm, ms / 3, 3 * bytes / ms / 1e6);
+  return 0;
+}
+
 __global__ void row_write(double4 *mu, int64_t n4) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
     st256((double2 *)(mu + i), 1.0, 2.0, 3.0, (double)i);
@@ -104,18 +153,16 @@ int main() {
     printf("%-28s bpsm=%d  %.3f ms  %.1f GB/s\n", "contiguous read (half)", bpsm, ms / 3, 3 * bytes / 2 / ms / 1e6);
   }
   for (int bpsm : {1, 2}) {
-    run<2, 1>(mu, logd, bpsm, "seg 32B");
     run<2, 1, false, true>(mu, logd, bpsm, "seg 32B desync");
-    run<2, 2, true>(mu, logd, bpsm, "seg 32B block-split 2");
-    run<2, 2, true, true>(mu, logd, bpsm, "seg 32B block-split 2 desync");
-    run<4, 1>(mu, logd, bpsm, "seg 64B");
+    rung<2, 1, 4>(mu, logd, bpsm, "seg 32B grouped 4");
+    rung<2, 2, 4>(mu, logd, bpsm, "seg 32B block-split 2 grouped 4");
+    rung<1, 1, 8>(mu, logd, bpsm, "seg 16B grouped 8");
+    rung<1, 2, 8>(mu, logd, bpsm, "seg 16B block-split 2 grouped 8");
     run<4, 1, false, true>(mu, logd, bpsm, "seg 64B desync");
-    run<4, 2, true>(mu, logd, bpsm, "seg 64B block-split 2");
-    run<4, 2, true, true>(mu, logd, bpsm, "seg 64B block-split 2 desync");
-    run<4, 4, true, true>(mu, logd, bpsm, "seg 64B block-split 4 desync");
+    rung<4, 1, 2>(mu, logd, bpsm, "seg 64B grouped 2");
+    rung<4, 2, 2>(mu, logd, bpsm, "seg 64B block-split 2 grouped 2");
     run<8, 1, false, true>(mu, logd, bpsm, "seg 128B desync");
-    run<8, 2, true, true>(mu, logd, bpsm, "seg 128B block-split 2 desync");
-    run<8, 4, true, true>(mu, logd, bpsm, "seg 128B block-split 4 desync");
+    rung<8, 8, 1>(mu, logd, bpsm, "seg 128B block-split 8");
   }
   return 0;
 }
