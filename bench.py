@@ -10,7 +10,9 @@ steps.  `value` = seconds per reconstruction with counts resident in HBM
 (CUDA events, max over ranks); `e2e` = the same reconstruction through the
 public streaming API from pinned HOST counts (H2D inside the timed region)
 with mu read back to the host.  `--impl reference` times the reference
-algorithm's CPU port (oracle/, kind "port") on the host cores.
+algorithm's CPU port (oracle/, kind "port") on the host cores, one full
+reconstruction measured in K pieces, with the real reference package timed
+beside it at n = 4..12.
 """
 
 from __future__ import annotations
@@ -109,7 +111,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the reference algorithm's C port on bounded samples
+# CPU reference timings (measured, never extrapolated from a cost model)
 # ---------------------------------------------------------------------------
 
 def workload_name(args) -> str:
@@ -118,54 +120,194 @@ def workload_name(args) -> str:
             f"{args.shots} shots/setting, seed {args.seed}, one reconstruction (steps i+ii) per step")
 
 
-def baseline_settings(n: int) -> int:
-    """Settings in the bounded step-(i) sample (about 10-20 s of single-node CPU work at n = 14)."""
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def device_record_rows(state_kind: str, n: int, shots: int, seed: int, lo: int, hi: int, out=None, state_seed=0):
+    """Rows [lo, hi) of the C-config record, drawn by the device generator (the same
+    record the B200 arm reconstructs) and copied to host memory — input preparation
+    only, outside every CPU timed region."""
+    import torch
+
+    if not torch.cuda.is_available():
+        # CPU-only containers (the bench's own CPU tests): the oracle's GHZ sampler
+        # (numpy Philox per setting, simulate.py:216-242) at small n
+        from oracle import lre_oracle as O
+
+        if state_kind != "ghz":
+            raise RuntimeError(f"no GPU: only GHZ records can be drawn on the host, not {state_kind}")
+        rows = O.sample_ghz_counts(n, shots, seed, lo, hi)
+        if out is None:
+            return rows
+        out[: hi - lo].copy_(torch.from_numpy(rows.astype(np.uint16 if shots <= 65535 else np.int32)))
+        return out[: hi - lo].numpy()
+
+    import paper_1602_08604_b200 as lre
+    from paper_1602_08604_b200.simulate import generate_device_counts
+
+    st = lre.StateDescriptor(state_kind, n, state_seed=state_seed)
+    dev = generate_device_counts(st, shots, seed=seed, w_begin=lo, w_end=hi)
+    if out is None:
+        return dev.cpu().numpy()
+    out[: hi - lo].copy_(dev)
+    del dev
+    return out[: hi - lo].numpy()
+
+
+# the parity configs of BASELINE.json timed on the CPU: (n, state, shots, state_seed)
+PER_N = [(4, "ghz", 1000, 0), (8, "w", 1000, 0), (10, "random", 1000, 8604), (12, "ghz", 1000, 0)]
+
+
+def _import_reference():
+    """The unmodified reference package (pip-installed into baseline/_ref, numba cache in /tmp)."""
+    path = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "pauli_lre")):
+        return None, "baseline/_ref is not installed (python -m pip install --no-index --no-deps --target baseline/_ref <copy of /root/reference/pkg>)"
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join("/tmp", "lre_numba_cache"))
+    if path not in sys.path:
+        sys.path.insert(0, path)
+    try:
+        import pauli_lre.pipeline as P
+        import pauli_lre.records as R
+        return (P, R), None
+    except Exception as exc:  # numba or numpy missing on the box
+        return None, f"{type(exc).__name__}: {str(exc)[:120]}"
+
+
+def reference_per_n(configs=PER_N, repeats: int = 3):
+    """The real reference (pauli_lre.pipeline.step_one_least_squares with all host cores +
+    step_two_assemble, workers=1, the faster setting for its numpy step ii) on the
+    configs' records, with the reference's own methodology (bench.py:18-37): one
+    discarded warm-up, median of `repeats`.  Returns a list of rows."""
+    mods, why = _import_reference()
     threads = os.cpu_count() or 1
-    d = 1 << n
-    S = max(threads * 4, min(3**n // 8, int(2e6 // d) * threads))
-    return min(S, 3**n // 2)
+    rows = []
+    for n, kind, shots, sseed in configs:
+        counts = device_record_rows(kind, n, shots, 1602, 0, 3**n, state_seed=sseed)
+        row = {"n": n, "state": kind, "shots": shots, "cores": threads}
+        if mods is not None:
+            P, R = mods
+            rec = R.MeasurementRecord(n=n, shots=shots, counts=counts)
+            rec.validate()
+            t1s, t2s = [], []
+            for rep in range(repeats + 1):
+                a = time.perf_counter()
+                theta = P.step_one_least_squares(rec, workers=threads)
+                b = time.perf_counter()
+                P.step_two_assemble(theta, workers=1)
+                c = time.perf_counter()
+                if rep:
+                    t1s.append(b - a)
+                    t2s.append(c - b)
+            row.update(kind="reference", t_step1_s=statistics.median(t1s), t_step2_s=statistics.median(t2s))
+            row["t_s"] = row["t_step1_s"] + row["t_step2_s"]
+        else:
+            row.update(kind="reference", unavailable=why)
+        # the C port beside it (same records, same methodology)
+        from oracle import c_oracle as C
+
+        tp = []
+        for rep in range(repeats + 1):
+            a = time.perf_counter()
+            theta = C.step_one(counts, n, shots, threads)
+            mu = np.empty((1 << n, 1 << n), dtype=np.complex128)
+            C.step_two_scatter(theta, n, 0, 1 << n, mu, threads)
+            if rep:
+                tp.append(time.perf_counter() - a)
+        row["port_t_s"] = statistics.median(tp)
+        rows.append(row)
+    return rows
 
 
-def cpu_baseline(n: int, shots: int, seed: int, counts_rows=None, budget_s: float = 20.0):
-    """Seconds of the reference LRE (steps i+ii) on the host cores, from a bounded sample.
+def port_tiled(n: int, shots: int, seed: int, state_kind: str, steps: int, warmup: int):
+    """One full C5 reconstruction by the C port of the reference (oracle/lre_oracle.c:
+    per-setting WHT + scatter into per-worker 4^n partials, ordered merge, Gram
+    division; step (ii) per-mask complex WHT + XOR-diagonal scatter), measured in
+    `steps` pieces: step k = step (i) over settings shard k (the partials persist
+    across shards) and step (ii) over masks shard k; the merge + Gram division is
+    part of the last step-(i) piece.  Nothing is extrapolated: the sum of the step
+    times is the measured wall time of one complete reconstruction on all host
+    cores.  The shard counts come from the device generator (untimed)."""
+    import torch
 
-    Step (i): the C port of the reference (oracle/lre_oracle.c: per-setting
-    WHT + scatter into private per-worker 4^n partials, ordered merge,
-    pipeline.py:62-138) on 2S sampled settings, as a cost model: one-time
-    fixed cost (zero-filling the workers' partials + merge) + steady-state
-    seconds per setting per worker x 3^n / workers
-    (lre_oracle_step1_cost; validated against full runs, see
-    profiles/README.md).  Step (ii): per-mask cost on M masks extrapolated to
-    2^n masks (pipeline.py:141-161).
-    """
     from oracle import c_oracle as C
-    from oracle import lre_oracle as O
 
+    C.build()
     threads = os.cpu_count() or 1
-    d = 1 << n
-    S = baseline_settings(n)
-    rows = counts_rows if counts_rows is not None and counts_rows.shape[0] >= 2 * S else \
-        O.sample_ghz_counts(n, shots, seed, 0, 2 * S)
-    fixed, per = C.step1_cost(rows[: 2 * S], n, shots, 0, threads)
-    t_step1 = fixed + per * 3**n / threads
-    theta = np.random.default_rng(0).standard_normal(4**n) * 2.0 ** (-n)
-    M = max(threads, min(d, int(4e6 // d) * threads // 4 or threads))
-    t0 = time.perf_counter()
-    C.step_two_masks(theta, n, 0, M, threads)
-    t_m = time.perf_counter() - t0
-    t_step2 = t_m / M * d
-    return {
-        "value": t_step1 + t_step2,
-        "unit": "s",
-        "cores": threads,
-        "kind": "port",
-        "sample": (f"n={n} GHZ, step (i) on {2 * S} of {3**n} settings: fixed {fixed:.2f} s (zeroing {threads} private "
-                   f"4^n partials + ordered merge) + {per * 1e6:.1f} us per setting per worker (steady state); "
-                   f"step (ii) on {M} of {d} masks; C port of _kernels.accumulate_fast + step_two_assemble, "
-                   f"{threads} threads"),
-        "t_step1_s": t_step1,
-        "t_step2_s": t_step2,
-    }
+    settings, d = 3**n, 1 << n
+    bounds = [settings * k // steps for k in range(steps + 1)]
+    mbounds = [d * k // steps for k in range(steps + 1)]
+    width = max(b - a for a, b in zip(bounds[:-1], bounds[1:]))
+    host = torch.empty((width, d), dtype=torch.uint16 if shots <= 65535 else torch.int32,
+                       pin_memory=torch.cuda.is_available())
+    # warm-up: the same code on a throw-away accumulator (thread pool, first touch of the shard buffer)
+    rows = device_record_rows(state_kind, n, shots, seed, 0, min(settings, 64), out=host)
+    for _ in range(max(1, warmup)):
+        w = C.Step1Accumulator(n, shots, threads)
+        w.add(rows, 0)
+        w.close()
+    acc = C.Step1Accumulator(n, shots, threads)
+    t_i, t_ii = [], []
+    for k in range(steps):
+        rows = device_record_rows(state_kind, n, shots, seed, bounds[k], bounds[k + 1], out=host)
+        a = time.perf_counter()
+        acc.add(rows, bounds[k])
+        t_i.append(time.perf_counter() - a)
+    a = time.perf_counter()
+    theta = acc.finish()
+    t_merge = time.perf_counter() - a
+    acc.close()
+    del host
+    mu = np.empty((d, d), dtype=np.complex128)
+    for k in range(steps):
+        a = time.perf_counter()
+        C.step_two_scatter(theta, n, mbounds[k], mbounds[k + 1], mu, threads)
+        t_ii.append(time.perf_counter() - a)
+    per_step = [t_i[k] + t_ii[k] + (t_merge if k == steps - 1 else 0.0) for k in range(steps)]
+    return {"per_step_s": per_step, "t_step1_s": sum(t_i) + t_merge, "t_step2_s": sum(t_ii), "t_merge_s": t_merge,
+            "value": sum(per_step), "cores": threads, "theta_head": theta[:4].tolist()}
+
+
+def cpu_baseline(n: int, shots: int, seed: int, state_kind: str, fraction: int = 16):
+    """The b200 arm's reported CPU baseline: the C port on a bounded sample of the C5
+    workload — the first 1/`fraction` of the settings (step i, fresh partials) and of
+    the masks (step ii) — plus the real reference at the small configs.  value =
+    the measured sample seconds x `fraction` (the bench's reference arm measures the
+    full reconstruction; this line only sizes it within the bench's time budget)."""
+    from oracle import c_oracle as C
+
+    C.build()
+    threads = os.cpu_count() or 1
+    settings, d = 3**n, 1 << n
+    s_hi, m_hi = settings // fraction, d // fraction
+    rows = device_record_rows(state_kind, n, shots, seed, 0, s_hi)
+    a = time.perf_counter()
+    acc = C.Step1Accumulator(n, shots, threads)
+    acc.add(rows, 0)
+    theta = acc.finish()
+    acc.close()
+    t1 = time.perf_counter() - a
+    del rows
+    mu = np.empty((d, d), dtype=np.complex128)
+    a = time.perf_counter()
+    C.step_two_scatter(theta, n, 0, m_hi, mu, threads)
+    t2 = time.perf_counter() - a
+    del mu, theta
+    per_n = reference_per_n(PER_N[:3], repeats=1)
+    return {"value": (t1 + t2) * fraction, "unit": "s", "cores": threads, "kind": "port",
+            "sample": (f"n={n} {state_kind.upper()} C5 record: C port step (i) on settings [0, {s_hi}) of {settings} "
+                       f"({t1:.2f} s incl. zeroing the {threads} worker partials, merge and Gram division) and step "
+                       f"(ii) on masks [0, {m_hi}) of {d} ({t2:.2f} s); value = sample x {fraction}. The full, "
+                       f"unextrapolated reconstruction is the --impl reference line."),
+            "cpu_model": cpu_model(), "per_n": per_n}
 
 
 # ---------------------------------------------------------------------------
@@ -380,8 +522,10 @@ def run_b200(args):
 
     base = None
     if not args.no_cpu_baseline:
-        S = baseline_settings(n)
-        base = cpu_baseline(n, shots, seed, counts[: 2 * S].cpu().numpy())
+        try:
+            base = cpu_baseline(n, shots, seed, args.state)
+        except Exception as exc:
+            base = {"value": None, "error": f"{type(exc).__name__}: {str(exc)[:160]}"}
 
     plan = lre.LREPlan(n, shots, dev)
     s = torch.cuda.current_stream(dev)
@@ -686,36 +830,42 @@ def _mem_available():
 # ---------------------------------------------------------------------------
 
 def run_reference(args):
+    """`bench.py --impl reference`: the reference's CPU LRE on this box's host cores, same
+    metric / unit / config as the B200 arm.  The K timed steps are K consecutive pieces
+    of ONE full C5 reconstruction by the C port of the reference (port_tiled; the
+    reference is Python + numba and compiles to nothing here, so per the tier rules
+    the port is the arm), value = their sum = seconds per reconstruction, measured.
+    The real reference package (pauli_lre from baseline/_ref, numba) is timed beside
+    it on the parity configs n = 4, 8, 10, 12 (cpu_baseline.per_n).  Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import torch
+
+    if torch.cuda.is_available():
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     n, shots, seed = args.n, args.shots, args.seed
-    from oracle import c_oracle as C
-
-    from oracle import lre_oracle as O
-
-    C.build()
-    # one bounded sample of the workload per step; the counts sample is drawn
-    # once, and at most 6 steps are timed so the arm ends within minutes for
-    # any --steps (the median is reported; `steps` says how many were timed)
-    rows = O.sample_ghz_counts(n, shots, seed, 0, 2 * baseline_settings(n))
-    warm, timed = min(1, max(0, args.warmup)), max(1, min(args.steps, 6))
-    vals = []
-    last = None
-    for i in range(warm + timed):
-        last = cpu_baseline(n, shots, seed, rows)
-        if i >= warm:
-            vals.append(last["value"])
-    v = statistics.median(vals)
+    t_start = time.perf_counter()
+    tiled = port_tiled(n, shots, seed, args.state, max(1, args.steps), args.warmup)
+    per_n = reference_per_n() if not args.no_per_n and torch.cuda.is_available() else []
+    v = tiled["value"]
+    k = len(tiled["per_step_s"])
     line = {
-        "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": len(vals), "warmup": args.warmup,
-        "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic: GHZ multinomial counts (numpy Philox per setting, simulate.py:216-242)",
+        "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": k, "warmup": args.warmup,
+        "ms_per_step": v / k * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic: the B200 arm's C5 record (device generator, Philox4x32-10 per "
+                                "(seed, setting)), copied to host memory shard by shard outside the timed region",
         "config": {"workload": workload_name(args), "n": n, "state": args.state, "shots": shots,
-                   "counts": "host-resident sample, see cpu_baseline.sample"},
+                   "counts": "uint16 host shards (pinned), one per step"},
         "impl": "reference",
-        "cpu_baseline": {k: last[k] for k in ("value", "unit", "cores", "kind", "sample")} | {"value": v},
+        "cpu_baseline": {"value": v, "unit": "s", "cores": tiled["cores"], "kind": "port",
+                         "sample": (f"the whole workload: step k of {k} = step (i) over settings shard k (worker "
+                                    f"partials persist across shards) + step (ii) over masks shard k; merge + Gram "
+                                    f"division in the last step; t_step1 {tiled['t_step1_s']:.2f} s, t_step2 "
+                                    f"{tiled['t_step2_s']:.2f} s; C port of pipeline.py:62-161, all host threads"),
+                         "cpu_model": cpu_model(), "per_step_s": tiled["per_step_s"], "per_n": per_n},
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_start,
     }
     print(json.dumps(line))
 
@@ -736,6 +886,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-step3", action="store_true", help="skip the separately timed step (iii) eigen-projection")
     ap.add_argument("--force-dist", action="store_true", help="run the torch.distributed path even at world size 1")
+    ap.add_argument("--no-per-n", action="store_true", help="reference arm: skip the per-n table of the real reference")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

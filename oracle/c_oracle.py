@@ -36,6 +36,12 @@ def lib():
         L.lre_oracle_step2_masks.argtypes = [vp, c_int, i64, i64, c_int, vp]
         L.lre_oracle_max_threads.restype = c_int
         L.lre_oracle_step1_cost.argtypes = [vp, c_int, c_int, i64, i64, i64, c_int, vp, vp]
+        L.lre_oracle_acc_new.restype = vp
+        L.lre_oracle_acc_new.argtypes = [c_int, i64, c_int]
+        L.lre_oracle_acc_free.argtypes = [vp]
+        L.lre_oracle_acc_add.argtypes = [vp, vp, c_int, i64, i64]
+        L.lre_oracle_acc_finish.argtypes = [vp, vp]
+        L.lre_oracle_step2_scatter.argtypes = [vp, c_int, i64, i64, c_int, vp]
         _lib = L
     return _lib
 
@@ -107,3 +113,41 @@ def step1_cost(counts: np.ndarray, n: int, shots: int, w_begin: int = 0, threads
     if rc:
         raise MemoryError("oracle step1 allocation failed")
     return fixed.value, per.value
+
+
+class Step1Accumulator:
+    """Step (i) in setting shards with persistent worker partials (lre_oracle_acc_*):
+    add(rows, w_begin) for each shard, then finish() -> theta (merge + Gram division)."""
+
+    def __init__(self, n: int, shots: int, threads=None):
+        self.n = n
+        self.h = lib().lre_oracle_acc_new(n, int(shots), _threads(threads))
+        if not self.h:
+            raise MemoryError("oracle accumulator allocation failed")
+
+    def add(self, counts: np.ndarray, w_begin: int) -> None:
+        counts = np.ascontiguousarray(counts)
+        if lib().lre_oracle_acc_add(self.h, counts.ctypes.data, _DTYPES[counts.dtype], int(w_begin),
+                                    int(w_begin) + counts.shape[0]):
+            raise MemoryError("oracle step1 allocation failed")
+
+    def finish(self, out: np.ndarray | None = None) -> np.ndarray:
+        theta = np.empty(4**self.n) if out is None else out
+        lib().lre_oracle_acc_finish(self.h, theta.ctypes.data)
+        return theta
+
+    def close(self) -> None:
+        if self.h:
+            lib().lre_oracle_acc_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+def step_two_scatter(theta: np.ndarray, n: int, m_begin: int, m_end: int, mu: np.ndarray, threads=None) -> None:
+    """Masks [m_begin, m_end) of step (ii) written into the dense mu (complex128, d x d)."""
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    if lib().lre_oracle_step2_scatter(theta.ctypes.data, n, int(m_begin), int(m_end), _threads(threads),
+                                      mu.ctypes.data):
+        raise MemoryError("oracle step2 allocation failed")

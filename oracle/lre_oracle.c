@@ -342,3 +342,141 @@ int lre_oracle_step2_masks(const double *theta, int n, int64_t m_begin, int64_t 
 }
 
 int lre_oracle_max_threads(void) { return omp_get_max_threads(); }
+
+/*
+ * Streaming form of lre_oracle_step1_raw for bench.py's reference arm: the
+ * workers' private 4**n partials persist across setting shards, so timing the
+ * shards of [0, 3**n) one after another and then the ordered merge + Gram
+ * division (pipeline.py:133-138) is one full step (i), measured in pieces.
+ * Each shard is split over the workers with np.linspace bounds (pipeline.py:62-65).
+ */
+typedef struct {
+    int n, threads;
+    int64_t shots;
+    double **partials;
+} lre_oracle_acc;
+
+void *lre_oracle_acc_new(int n, int64_t shots, int threads) {
+    lre_oracle_acc *acc = (lre_oracle_acc *)calloc(1, sizeof(lre_oracle_acc));
+    if (!acc) return NULL;
+    acc->n = n;
+    acc->shots = shots;
+    acc->threads = threads < 1 ? 1 : threads;
+    acc->partials = (double **)calloc((size_t)acc->threads, sizeof(double *));
+    if (!acc->partials) {
+        free(acc);
+        return NULL;
+    }
+    return acc;
+}
+
+void lre_oracle_acc_free(void *h) {
+    lre_oracle_acc *acc = (lre_oracle_acc *)h;
+    if (!acc) return;
+    for (int i = 0; i < acc->threads; ++i) free(acc->partials[i]);
+    free(acc->partials);
+    free(acc);
+}
+
+/* settings [w_begin, w_end) of a counts block whose first row is w_begin (_step_one_chunk, pipeline.py:74-90) */
+int lre_oracle_acc_add(void *h, const void *counts, int dtype, int64_t w_begin, int64_t w_end) {
+    lre_oracle_acc *acc = (lre_oracle_acc *)h;
+    const int n = acc->n, threads = acc->threads;
+    const int64_t d = (int64_t)1 << n;
+    const int64_t size = (int64_t)1 << (2 * n);
+    const double scale = pow(2.0, -n / 2.0);
+    const double fshots = (double)acc->shots;
+    const int64_t total = w_end - w_begin;
+    int failed = 0;
+#pragma omp parallel num_threads(threads)
+    {
+        int tid = omp_get_thread_num();
+        int64_t a = (int64_t)((double)total * tid / threads);
+        int64_t b = (int64_t)((double)total * (tid + 1) / threads);
+        if (!acc->partials[tid]) acc->partials[tid] = (double *)calloc((size_t)size, sizeof(double));
+        double *raw = acc->partials[tid];
+        double *buf = (double *)malloc((size_t)d * sizeof(double));
+        int64_t *locs = (int64_t *)malloc((size_t)d * sizeof(int64_t));
+        int64_t pd[64];
+        if (!raw || !buf || !locs) {
+#pragma omp atomic write
+            failed = 1;
+        } else {
+            for (int64_t r = a; r < b; ++r) {
+                const int64_t row = r * d;
+                for (int64_t s = 0; s < d; ++s) buf[s] = load_count(counts, dtype, row + s) / fshots;
+                wht_inplace(buf, d);
+                place_digits(w_begin + r, n, pd);
+                fill_locations(pd, n, locs);
+                for (int64_t t = 0; t < d; ++t) raw[locs[t]] += buf[t] * scale;
+            }
+        }
+        free(buf);
+        free(locs);
+    }
+    return failed;
+}
+
+/* ordered merge of the partials (pipeline.py:135-137) and the Gram division (:138) */
+int lre_oracle_acc_finish(void *h, double *theta_out) {
+    lre_oracle_acc *acc = (lre_oracle_acc *)h;
+    const int threads = acc->threads;
+    const int64_t size = (int64_t)1 << (2 * acc->n);
+    if (acc->partials[0]) memcpy(theta_out, acc->partials[0], (size_t)size * sizeof(double));
+    else memset(theta_out, 0, (size_t)size * sizeof(double));
+    for (int i = 1; i < threads; ++i) {
+        const double *p = acc->partials[i];
+        if (!p) continue;
+#pragma omp parallel for num_threads(threads) schedule(static)
+        for (int64_t j = 0; j < size; ++j) theta_out[j] += p[j];
+    }
+    lre_oracle_gram_divide(theta_out, acc->n);
+    return 0;
+}
+
+/* step (ii) for masks [m_begin, m_end) scattered into the dense row-major mu
+ * (d x d interleaved complex): mu[r, r ^ m] (pipeline.py:154-160) */
+int lre_oracle_step2_scatter(const double *theta, int n, int64_t m_begin, int64_t m_end, int threads, double *mu) {
+    const int64_t d = (int64_t)1 << n;
+    const double scale = pow(2.0, -n / 2.0);
+    if (threads < 1) threads = 1;
+    int failed = 0;
+#pragma omp parallel num_threads(threads)
+    {
+        double *re = (double *)malloc((size_t)d * sizeof(double));
+        double *im = (double *)malloc((size_t)d * sizeof(double));
+        if (!re || !im) {
+#pragma omp atomic write
+            failed = 1;
+        } else {
+#pragma omp for schedule(static)
+            for (int64_t m = m_begin; m < m_end; ++m) {
+                for (int64_t a = 0; a < d; ++a) {
+                    int64_t idx = 0;
+                    for (int k = 0; k < n; ++k) {
+                        int sh = n - 1 - k;
+                        int mb = (int)((m >> sh) & 1), ab = (int)((a >> sh) & 1);
+                        idx = idx * 4 + (mb ? 1 + ab : 3 * ab);
+                    }
+                    double v = theta[idx];
+                    switch (__builtin_popcountll((unsigned long long)(a & m)) & 3) {
+                    case 0: re[a] = v; im[a] = 0.0; break;
+                    case 1: re[a] = 0.0; im[a] = -v; break;
+                    case 2: re[a] = -v; im[a] = 0.0; break;
+                    default: re[a] = 0.0; im[a] = v; break;
+                    }
+                }
+                wht_inplace(re, d);
+                wht_inplace(im, d);
+                for (int64_t r = 0; r < d; ++r) {
+                    double *o = mu + 2 * (r * d + (r ^ m));
+                    o[0] = re[r] * scale;
+                    o[1] = im[r] * scale;
+                }
+            }
+        }
+        free(re);
+        free(im);
+    }
+    return failed;
+}
