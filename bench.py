@@ -151,10 +151,20 @@ def device_record_rows(state_kind: str, n: int, shots: int, seed: int, lo: int, 
         return out[: hi - lo].numpy()
 
     import paper_1602_08604_b200 as lre
-    from paper_1602_08604_b200.simulate import generate_device_counts
+    from paper_1602_08604_b200.simulate import dense_to_theta, generate_counts_from_theta, generate_device_counts
 
-    st = lre.StateDescriptor(state_kind, n, state_seed=state_seed)
-    dev = generate_device_counts(st, shots, seed=seed, w_begin=lo, w_end=hi)
+    if state_kind == "random":
+        # C3: the reference's Ginibre state _random_density(n, seed) (simulate.py:105-111),
+        # beyond the StateDescriptor cap of n <= 8, sampled from its Pauli coefficients
+        d = 1 << n
+        rng = np.random.default_rng(state_seed)
+        g = rng.standard_normal((d, d)) + 1j * rng.standard_normal((d, d))
+        rho = g @ g.conj().T
+        rho /= np.trace(rho).real
+        dev = generate_counts_from_theta(dense_to_theta(rho, as_tensor=True), n, shots, seed, lo, hi)
+    else:
+        st = lre.StateDescriptor(state_kind, n, state_seed=state_seed)
+        dev = generate_device_counts(st, shots, seed=seed, w_begin=lo, w_end=hi)
     if out is None:
         return dev.cpu().numpy()
     out[: hi - lo].copy_(dev)

@@ -5,7 +5,10 @@
  * Every pointer marked (device) is device memory owned by the caller; every
  * call is asynchronous on the given cudaStream_t (pass 0 for the legacy
  * stream) and returns an lre_status.  The library allocates nothing and keeps
- * no hidden state except a launch counter.  Host code (Python via ctypes, see
+ * no hidden state except a launch counter and a per-device cache of the SM
+ * count (read-only after the first call); epilogue factors travel with each
+ * launch.  lre_generate_counts with exact != 0 synchronises `stream` (it
+ * checks that the state is dyadic).  Host code (Python via ctypes, see
  * INTEGRATION.md) owns memory, streams and the NCCL communicator.
  *
  * Layout conventions (reference pauli.py:1-13): qubit 1 is the most
@@ -93,12 +96,44 @@ int lre_step1_num_passes(int n, int64_t shots);
  * first fold pass of chunk [w_begin, w_end) (rows of `counts`) into a
  * full-range workspace (size from lre_step1_workspace(n, shots, 0, 3^n));
  * after every chunk has been staged once, lre_step1_finish runs the remaining
- * passes.  Requires lre_step1_num_passes(n, shots) >= 2.
+ * passes.  When lre_step1_num_passes(n, shots) == 1 (n <= 2, 6, 7) the shard
+ * quantum is the whole record, so the only chunk is [0, 3^n).
  */
 int lre_step1_stage(const void *counts, int count_dtype, int n, int64_t shots, int64_t w_begin, int64_t w_end,
                     void *workspace, size_t workspace_bytes, lre_stream_t stream);
 int lre_step1_finish(void *workspace, size_t workspace_bytes, int n, int64_t shots, void *out, int out_kind,
                      int layout, lre_stream_t stream);
+
+/*
+ * Step (i) from fp64 frequencies: the reference's source protocol
+ * (pipeline.py:42-59,84 — any source with .frequencies(a, b), e.g.
+ * ExactFrequencies; records.py:62-64 for counts/shots).  Streaming only:
+ * lre_step1_f64_stage folds the chunk of settings [w_begin, w_end) (rows of
+ * `freq`, device fp64, 2^n per row; w_begin a multiple of
+ * lre_step1_f64_quantum(n), w_end too unless it is 3^n) into `workspace`
+ * (its first passes run in `scratch`); after every chunk has been staged once,
+ * lre_step1_f64_finish writes theta (fp64, `layout`).  Sizes:
+ * lre_step1_f64_workspace(n, max chunk rows, &workspace, &scratch).
+ * Replaces pipeline.py:116-138 for non-integer sources.
+ */
+int lre_step1_f64_workspace(int n, int64_t chunk_rows, size_t *workspace_bytes, size_t *scratch_bytes);
+int64_t lre_step1_f64_quantum(int n);
+int lre_step1_f64_stage(const double *freq, int n, int64_t w_begin, int64_t w_end, void *workspace,
+                        size_t workspace_bytes, void *scratch, size_t scratch_bytes, lre_stream_t stream);
+int lre_step1_f64_finish(void *workspace, size_t workspace_bytes, int n, double *theta, int layout,
+                         lre_stream_t stream);
+
+/*
+ * Exact outcome probabilities (device fp64, rows x 2^n) of settings
+ * [w_begin, w_end) for the state with Pauli coefficients theta (device,
+ * NATURAL): 2^{-n/2} WHT of theta on each setting's support — the
+ * reference's _theta_probability_block / theta_to_probabilities
+ * (simulate.py:141-151); clip != 0 clamps to [0, 1] as probabilities_block
+ * does for random states (:176-177, i.e. ExactFrequencies.frequencies).
+ * n <= 12.
+ */
+int lre_theta_probabilities(const double *theta, int n, int64_t w_begin, int64_t w_end, int clip, double *out,
+                            lre_stream_t stream);
 
 /*
  * int64 numerators (device, entries [begin, end) of `layout`) -> fp64 theta

@@ -35,6 +35,11 @@ _SIGNATURES = {
     "lre_step1": (_i, [_vp, _i, _i, _i64, _i64, _i64, _vp, _sz, _vp, _i, _i, _vp]),
     "lre_step1_stage": (_i, [_vp, _i, _i, _i64, _i64, _i64, _vp, _sz, _vp]),
     "lre_step1_finish": (_i, [_vp, _sz, _i, _i64, _vp, _i, _i, _vp]),
+    "lre_step1_f64_workspace": (_i, [_i, _i64, ctypes.POINTER(_sz), ctypes.POINTER(_sz)]),
+    "lre_step1_f64_quantum": (_i64, [_i]),
+    "lre_step1_f64_stage": (_i, [_vp, _i, _i64, _i64, _vp, _sz, _vp, _sz, _vp]),
+    "lre_step1_f64_finish": (_i, [_vp, _sz, _i, _vp, _i, _vp]),
+    "lre_theta_probabilities": (_i, [_vp, _i, _i64, _i64, _i, _vp, _vp]),
     "lre_finalize": (_i, [_vp, _i, _i64, _i, _i64, _i64, _vp, _vp]),
     "lre_theta_relayout": (_i, [_vp, _i, _i, _vp, _vp]),
     "lre_assemble": (_i, [_vp, _i, _i, _i64, _i64, _vp, _vp]),

@@ -31,6 +31,14 @@ int step1_stage_impl(const void *counts, int dtype, int n, int64_t shots, int64_
 int step1_finish_impl(void *ws, size_t ws_bytes, int n, int64_t shots, void *out, int out_kind, int layout,
                       cudaStream_t stream);
 int step1_num_passes(int n, int64_t shots);
+size_t step1_f64_workspace(int n);
+size_t step1_f64_scratch(int n, int64_t rows);
+int64_t step1_f64_quantum(int n);
+int step1_f64_stage_impl(const double *freq, int n, int64_t w_begin, int64_t w_end, void *ws, size_t ws_bytes,
+                         void *scratch, size_t scratch_bytes, cudaStream_t stream);
+int step1_f64_finish_impl(void *ws, size_t ws_bytes, int n, double *theta, int layout, cudaStream_t stream);
+int theta_probabilities_impl(const double *theta, int n, int64_t w_begin, int64_t w_end, int clip, double *out,
+                             cudaStream_t s);
 int64_t shard_quantum(int n, int64_t shots);
 int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s);
 int validate_impl(const void *counts, int dtype, int n, int64_t rows, int64_t shots, int64_t *result,
@@ -135,6 +143,37 @@ int lre_step1_finish(void *workspace, size_t workspace_bytes, int n, int64_t sho
     if (layout != LRE_LAYOUT_NATURAL && layout != LRE_LAYOUT_MASK_MAJOR) return LRE_EINVAL;
     return lre::step1_finish_impl(workspace, workspace_bytes, n, shots, out, out_kind, layout,
                                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_step1_f64_workspace(int n, int64_t chunk_rows, size_t *ws_bytes, size_t *scratch_bytes) {
+    if (!valid_n(n) || !ws_bytes || !scratch_bytes || chunk_rows < 1) return LRE_EINVAL;
+    *ws_bytes = lre::step1_f64_workspace(n);
+    *scratch_bytes = lre::step1_f64_scratch(n, chunk_rows);
+    return LRE_OK;
+}
+
+int64_t lre_step1_f64_quantum(int n) { return valid_n(n) ? lre::step1_f64_quantum(n) : -1; }
+
+int lre_step1_f64_stage(const double *freq, int n, int64_t w_begin, int64_t w_end, void *workspace,
+                        size_t workspace_bytes, void *scratch, size_t scratch_bytes, lre_stream_t stream) {
+    if (!valid_n(n) || !freq) return LRE_EINVAL;
+    if (w_begin < 0 || w_end > pow3_i(n) || w_begin >= w_end) return LRE_EINVAL;
+    return lre::step1_f64_stage_impl(freq, n, w_begin, w_end, workspace, workspace_bytes, scratch, scratch_bytes,
+                                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_step1_f64_finish(void *workspace, size_t workspace_bytes, int n, double *theta, int layout,
+                         lre_stream_t stream) {
+    if (!valid_n(n) || !theta) return LRE_EINVAL;
+    if (layout != LRE_LAYOUT_NATURAL && layout != LRE_LAYOUT_MASK_MAJOR) return LRE_EINVAL;
+    return lre::step1_f64_finish_impl(workspace, workspace_bytes, n, theta, layout,
+                                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_theta_probabilities(const double *theta, int n, int64_t w_begin, int64_t w_end, int clip, double *out,
+                            lre_stream_t stream) {
+    if (!valid_n(n) || !theta || !out || w_begin < 0 || w_end < w_begin || w_end > pow3_i(n)) return LRE_EINVAL;
+    return lre::theta_probabilities_impl(theta, n, w_begin, w_end, clip, out, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int lre_finalize(const int64_t *num, int n, int64_t shots, int layout, int64_t begin, int64_t end, double *theta,

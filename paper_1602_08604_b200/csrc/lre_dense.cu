@@ -153,6 +153,54 @@ int dense_to_theta_impl(const double *rho, int n, double *theta, cudaStream_t s)
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
 }
 
+// exact outcome probabilities of settings [w_begin, w_end) (simulate.py:141-151 and
+// probabilities_block's random-state branch, :176-177): per setting, theta on the
+// setting's support, one WHT, * 2^{-n/2}, clipped to [0, 1]
+__global__ void __launch_bounds__(DENSE_THREADS) theta_prob_kernel(const double *__restrict__ theta, int n,
+                                                                   int64_t w_begin, int64_t w_end, int clip,
+                                                                   double *__restrict__ out) {
+    extern __shared__ double psm[];
+    const int d = 1 << n;
+    const double scale = exp2(-0.5 * n);
+    for (int64_t w = w_begin + blockIdx.x; w < w_end; w += gridDim.x) {
+        int ax[16];
+        {
+            int64_t x = w;
+            for (int k = n - 1; k >= 0; --k) {
+                ax[k] = (int)(x % 3);
+                x /= 3;
+            }
+        }
+        for (int mask = threadIdx.x; mask < d; mask += blockDim.x) {
+            uint64_t nat = 0;
+            for (int k = 0; k < n; ++k) {
+                const int dig = ((mask >> (n - 1 - k)) & 1) ? ax[k] + 1 : 0;
+                nat = (nat << 2) | (uint64_t)dig;
+            }
+            psm[mask] = __ldg(theta + nat);
+        }
+        __syncthreads();
+        smem_wht(psm, n);
+        double *row = out + (w - w_begin) * (int64_t)d;
+        for (int s = threadIdx.x; s < d; s += blockDim.x)
+            row[s] = clip ? fmin(fmax(scale * psm[s], 0.0), 1.0) : scale * psm[s];
+        __syncthreads();
+    }
+}
+
+int theta_probabilities_impl(const double *theta, int n, int64_t w_begin, int64_t w_end, int clip, double *out,
+                             cudaStream_t s) {
+    if (n < 1 || n > 12) return LRE_EUNSUPPORTED;
+    if (w_end <= w_begin) return LRE_OK;
+    const size_t smem = ((size_t)1 << n) * sizeof(double);
+    if (cudaFuncSetAttribute(theta_prob_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return LRE_ECUDA;
+    const int grid = (int)std::min<int64_t>(w_end - w_begin, (int64_t)num_sms() * 8);
+    theta_prob_kernel<<<grid, DENSE_THREADS, smem, s>>>(theta, n, w_begin, w_end, clip, out);
+    count_launch(1);
+    return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
+}
+
 template <typename T>
 static int gen_theta_t(const double *theta, int n, int64_t shots, uint64_t seed, int64_t w_begin, int64_t w_end,
                        void *out, cudaStream_t s) {

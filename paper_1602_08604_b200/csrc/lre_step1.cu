@@ -51,6 +51,18 @@ struct Final {
     Factors fac;  // theta = N * fac[zc] (lre_internal.cuh), staged in shared memory by the final kernels
 };
 
+// store a finished fp64 numerator (frequency sources: theta = N * fac[zc], fac from shots = 1)
+__device__ __forceinline__ void store_final(const Final &f, const double *sfac, uint64_t nat, double v) {
+    uint64_t pos = nat;
+    if (f.layout == LRE_LAYOUT_MASK_MAJOR) {
+        uint32_t m, a;
+        natural_to_ma(nat, m, a);
+        pos = ((uint64_t)m << f.n) | a;
+    }
+    const int zc = f.n - __popcll((nat | (nat >> 1)) & 0x5555555555555555ull);
+    reinterpret_cast<double *>(f.out)[pos] = v * sfac[zc];
+}
+
 // store a finished numerator at natural Pauli index `nat`; sfac = the staged fac table
 __device__ __forceinline__ void store_final(const Final &f, const double *sfac, uint64_t nat, int64_t v) {
     uint64_t pos = nat;
@@ -896,12 +908,19 @@ struct VArgs {
     Final f;
 };
 
-template <typename Tin>
-__device__ __forceinline__ int64_t vload(const Tin *p) {
-    return (int64_t)__ldcs(p);
+// final-store value: integers widen to int64 numerators, fp64 stays fp64
+template <typename Ta> __device__ __forceinline__ auto fin_val(Ta y) {
+    if constexpr (std::is_floating_point<Ta>::value) return (double)y;
+    else return (int64_t)y;
 }
-template <> __device__ __forceinline__ int64_t vload<uint8_t>(const uint8_t *p) { return (int64_t)*p; }
-template <> __device__ __forceinline__ int64_t vload<uint16_t>(const uint16_t *p) {
+
+template <typename Tin>
+__device__ __forceinline__ auto vload(const Tin *p) {
+    if constexpr (std::is_floating_point<Tin>::value) return __ldcs(p);
+    else return (int64_t)__ldcs(p);
+}
+template <> __device__ __forceinline__ auto vload<uint8_t>(const uint8_t *p) { return (int64_t)*p; }
+template <> __device__ __forceinline__ auto vload<uint16_t>(const uint16_t *p) {
     return (int64_t)__ldcs(reinterpret_cast<const unsigned short *>(p));
 }
 
@@ -1029,7 +1048,7 @@ __global__ void __launch_bounds__(128, Q == 1 ? VF1_MINB : 4) vfold_kernel(const
                     for (int d = 0; d < 4; ++d) out[(int64_t)d * a.V] = D[d];
                 } else {
 #pragma unroll
-                    for (int d = 0; d < 4; ++d) store_final(a.f, sfac, (uint64_t)(d * a.V + vv[u]), (int64_t)D[d]);
+                    for (int d = 0; d < 4; ++d) store_final(a.f, sfac, (uint64_t)(d * a.V + vv[u]), fin_val(D[d]));
                 }
             }
         }
@@ -1053,7 +1072,7 @@ __global__ void __launch_bounds__(128, Q == 1 ? VF1_MINB : 4) vfold_kernel(const
             Ta *out = reinterpret_cast<Ta *>(a.f.out) + ((A - a.ya0) * a.nB + B) * NOUT * V + v;
             vblock<Q, Ta>(ld, [&](int d, Ta y) { out[(int64_t)d * V] = y; });
         } else {
-            vblock<Q, Ta>(ld, [&](int d, Ta y) { store_final(a.f, sfac, (uint64_t)(d * V + v), (int64_t)y); });
+            vblock<Q, Ta>(ld, [&](int d, Ta y) { store_final(a.f, sfac, (uint64_t)(d * V + v), fin_val(y)); });
         }
     }
     }
@@ -1711,5 +1730,179 @@ size_t step1_workspace(int n, int64_t shots, int64_t w_begin, int64_t w_end) {
 // setting shards must align to the first pass's row groups; 3^min(n,7) works
 // for every plan (3^q1 divides it)
 int64_t shard_quantum(int n, int64_t /*shots*/) { return ipow(3, std::min(n, 7)); }
+
+// ===========================================================================
+// step (i) from fp64 frequencies (the reference's source protocol,
+// pipeline.py:42-59,84: any object with .frequencies(a, b); ExactFrequencies)
+// ===========================================================================
+// The same separable A^{(x)n} map in fp64: 2-qubit vfold passes (a final
+// 1-qubit pass for odd n).  Records of fp64 frequencies (8 B per entry, 627 GB
+// at n = 14) only ever exist chunk by chunk: lre_step1_f64_stage runs the
+// first s <= 3 passes of a chunk (its intermediates in `scratch`), the last of
+// them writing into the full-range level-s buffer of the workspace;
+// lre_step1_f64_finish runs the remaining passes.  theta = N * 2^{-n/2} / 3^zc
+// (make_factors with shots = 1: the frequencies are already normalised).
+struct F64Plan {
+    std::vector<int> q;  // qubits per pass
+    int staged = 0;      // passes run per chunk
+    int64_t quantum = 1; // chunk alignment (settings)
+    size_t ws_off[2] = {0, 0}, ws_bytes = 0;
+};
+
+static F64Plan f64_plan(int n) {
+    F64Plan pl;
+    int rem = n;
+    while (rem > 0) {
+        const int q = rem >= 2 ? 2 : 1;
+        pl.q.push_back(q);
+        rem -= q;
+    }
+    const int P = (int)pl.q.size();
+    pl.staged = P == 1 ? 0 : std::min(3, P - 1);
+    int S = 0;
+    for (int i = 0; i < pl.staged; ++i) S += pl.q[i];
+    pl.quantum = ipow(3, S);
+    // full-range levels s .. P-1 ping-pong in two buffers (level l: 6^(n-S_l) 4^S_l doubles)
+    size_t need[2] = {0, 0};
+    int done = S;
+    for (int p = pl.staged; p < P; ++p) {
+        const size_t lvl = (size_t)ipow(6, n - done) * (size_t)ipow(4, done) * sizeof(double);
+        need[(p - pl.staged) & 1] = std::max(need[(p - pl.staged) & 1], lvl);
+        done += pl.q[p];
+    }
+    pl.ws_off[0] = 0;
+    pl.ws_off[1] = (need[0] + 255) & ~(size_t)255;
+    pl.ws_bytes = pl.ws_off[1] + ((need[1] + 255) & ~(size_t)255);
+    return pl;
+}
+
+// chunk-local scratch for the first staged passes of a chunk of `rows` settings
+static size_t f64_scratch_bytes(const F64Plan &pl, int n, int64_t rows) {
+    size_t off = 0;
+    int done = 0;
+    int64_t r = rows;
+    for (int p = 0; p + 1 < pl.staged; ++p) {
+        done += pl.q[p];
+        r = (r + ipow(3, pl.q[p]) - 1) / ipow(3, pl.q[p]);
+        off += (((size_t)r * (size_t)ipow(2, n - done) * (size_t)ipow(4, done) * sizeof(double)) + 255) & ~(size_t)255;
+    }
+    return off;
+}
+
+static cudaError_t f64_pass(int q, const VArgs &a, bool fin, cudaStream_t s) {
+    const int64_t total = a.nA * a.nB * a.V;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + 127) / 128, (int64_t)num_sms() * 16));
+    if (q == 2) {
+        if (fin) vfold_kernel<2, double, double, true><<<(unsigned)blocks, 128, 0, s>>>(a);
+        else vfold_kernel<2, double, double, false><<<(unsigned)blocks, 128, 0, s>>>(a);
+    } else {
+        if (fin) vfold_kernel<1, double, double, true><<<(unsigned)blocks, 128, 0, s>>>(a);
+        else vfold_kernel<1, double, double, false><<<(unsigned)blocks, 128, 0, s>>>(a);
+    }
+    count_launch();
+    return cudaGetLastError();
+}
+
+static VArgs f64_args(int n, int done, int q, const void *in, int64_t xa0, int64_t alo, int64_t ahi, void *out,
+                      int64_t ya0, const Final &f) {
+    VArgs a;
+    a.in = in;
+    a.V = ipow(4, done);
+    a.ncol = ipow(2, n - done);
+    a.xa0 = xa0;
+    a.alo = alo;
+    a.ahi = ahi;
+    const int64_t q3 = ipow(3, q);
+    a.A0 = alo / q3;
+    a.nA = (ahi + q3 - 1) / q3 - a.A0;
+    a.ya0 = ya0;
+    a.nB = ipow(2, n - done - q);
+    a.logV = 2 * done;
+    a.lognB = n - done - q;
+    a.vf1_batch = 1;
+    a.f = f;
+    a.f.out = out;
+    return a;
+}
+
+size_t step1_f64_workspace(int n) { return f64_plan(n).ws_bytes; }
+size_t step1_f64_scratch(int n, int64_t rows) { return f64_scratch_bytes(f64_plan(n), n, rows); }
+int64_t step1_f64_quantum(int n) { return f64_plan(n).quantum; }
+
+int step1_f64_stage_impl(const double *freq, int n, int64_t w_begin, int64_t w_end, void *ws, size_t ws_bytes,
+                         void *scratch, size_t scratch_bytes, cudaStream_t stream) {
+    const F64Plan pl = f64_plan(n);
+    if (ensure_init() != cudaSuccess) return LRE_ECUDA;
+    if (ws_bytes < pl.ws_bytes || !ws) return LRE_ENOMEM;
+    if (scratch_bytes < f64_scratch_bytes(pl, n, w_end - w_begin)) return LRE_ENOMEM;
+    const int64_t settings = ipow(3, n);
+    if (w_begin % pl.quantum || (w_end % pl.quantum && w_end != settings)) return LRE_EINVAL;
+    if (pl.staged == 0) {  // n <= 2: the whole record is level 0 of the workspace
+        if (cudaMemcpyAsync((char *)ws + pl.ws_off[0] + (size_t)w_begin * ((size_t)1 << n) * sizeof(double), freq,
+                            (size_t)(w_end - w_begin) * ((size_t)1 << n) * sizeof(double), cudaMemcpyDeviceToDevice,
+                            stream) != cudaSuccess)
+            return LRE_ECUDA;
+        return LRE_OK;
+    }
+    Final f{};
+    f.kind = OUT_INTER;
+    f.n = n;
+    int done = 0;
+    int64_t lo = w_begin, hi = w_end;
+    const void *in = freq;
+    int64_t xa0 = w_begin;
+    size_t soff = 0;
+    for (int p = 0; p < pl.staged; ++p) {
+        const int q = pl.q[p];
+        const bool last = p + 1 == pl.staged;
+        const int64_t q3 = ipow(3, q);
+        const int64_t A0 = lo / q3, A1 = (hi + q3 - 1) / q3;
+        void *out;
+        int64_t ya0;
+        if (last) {
+            out = (char *)ws + pl.ws_off[0];
+            ya0 = 0;
+        } else {
+            out = (char *)scratch + soff;
+            ya0 = A0;
+            soff += (((size_t)(A1 - A0) * (size_t)ipow(2, n - done - q) * (size_t)ipow(4, done + q) * sizeof(double)) +
+                     255) & ~(size_t)255;
+        }
+        const VArgs a = f64_args(n, done, q, in, xa0, lo, hi, out, ya0, f);
+        if (f64_pass(q, a, false, stream) != cudaSuccess) return LRE_ECUDA;
+        in = out;
+        xa0 = ya0;
+        lo = A0;
+        hi = A1;
+        done += q;
+    }
+    return LRE_OK;
+}
+
+int step1_f64_finish_impl(void *ws, size_t ws_bytes, int n, double *theta, int layout, cudaStream_t stream) {
+    const F64Plan pl = f64_plan(n);
+    if (ensure_init() != cudaSuccess) return LRE_ECUDA;
+    if (ws_bytes < pl.ws_bytes || !ws) return LRE_ENOMEM;
+    const int P = (int)pl.q.size();
+    int done = 0;
+    for (int p = 0; p < pl.staged; ++p) done += pl.q[p];
+    Final f{};
+    f.n = n;
+    f.layout = layout;
+    f.shots = 1;
+    f.fac = make_factors(n, 1);
+    for (int p = pl.staged; p < P; ++p) {
+        const int q = pl.q[p];
+        const bool fin = p + 1 == P;
+        const void *in = (const char *)ws + pl.ws_off[(p - pl.staged) & 1];
+        void *out = fin ? (void *)theta : (void *)((char *)ws + pl.ws_off[(p - pl.staged + 1) & 1]);
+        f.kind = fin ? OUT_THETA : OUT_INTER;
+        const int64_t rows = ipow(3, n - done);
+        const VArgs a = f64_args(n, done, q, in, 0, 0, rows, out, 0, f);
+        if (f64_pass(q, a, fin, stream) != cudaSuccess) return LRE_ECUDA;
+        done += q;
+    }
+    return LRE_OK;
+}
 
 }  // namespace lre

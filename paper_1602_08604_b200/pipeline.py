@@ -15,10 +15,17 @@ is no CPU path).  ``workers`` is accepted for signature compatibility (the
 GPU decides its own parallelism); ``kernel`` accepts the reference names
 "fast" and "paper-direct" (both map to the same B200 kernels, their outputs
 being identical by construction in the reference as well) and "b200".
-Sources: ``MeasurementRecord`` (host counts; copied to HBM, validated on the
-device), ``DeviceRecord`` (counts already in HBM) or ``StateDescriptor``
-(exact noiseless record generated on the device; the reference's
-ExactFrequencies).  Outputs are numpy arrays by default; pass
+Sources (the reference's source protocol, pipeline.py:42-59,84):
+``MeasurementRecord`` (host counts; copied to HBM, validated on the device),
+``DeviceRecord`` / ``OutcomeRecord`` (counts or raw shots already in HBM),
+``StateDescriptor`` (the reference wraps it in ``ExactFrequencies``),
+``ExactFrequencies`` and any duck-typed object with ``.n``, ``.num_settings``
+and ``.frequencies(a, b)``.  Integer records run the exact integer folds;
+frequency sources run the fp64 folds (``lre_step1_f64_*``): exact
+probabilities of dyadic states are an exact integer record (shots = 2^n),
+other states' probabilities are computed on the device from their Pauli
+coefficients (n <= 12), and any other source's frequency blocks are streamed
+from the host in setting chunks.  Outputs are numpy arrays by default; pass
 ``as_tensor=True`` to keep torch CUDA tensors.
 """
 
@@ -30,7 +37,7 @@ import numpy as np
 
 from . import _lib, pauli
 from .records import DeviceRecord, MeasurementRecord, OutcomeRecord, compact_dtype, lre_dtype_of
-from .simulate import StateDescriptor, exact_record
+from .simulate import StateDescriptor, exact_record, probabilities_block, state_theta, theta_probabilities
 
 KERNELS = ("b200", "fast", "paper-direct")
 DENSE_PIPELINE_MAX_QUBITS = 14  # reference caps at 12 (pipeline.py:31); the B200 path lifts it
@@ -71,6 +78,44 @@ def _check_kernel(kernel: str) -> None:
 # ---------------------------------------------------------------------------
 # sources
 # ---------------------------------------------------------------------------
+
+class ExactFrequencies:
+    """Infinite-shot frequency source backed by exact probabilities (pipeline.py:42-51).
+
+    ``frequencies(a, b)`` returns host fp64 blocks (the protocol); the pipeline
+    itself never round-trips them through the host: dyadic states become their
+    exact integer record, others are evaluated on the device."""
+
+    def __init__(self, state: StateDescriptor):
+        self.state = state
+        self.n = state.n
+        self.num_settings = 3**state.n
+
+    def frequencies(self, start: int, stop: int) -> np.ndarray:
+        return probabilities_block(self.state, start, stop)
+
+
+def _is_frequency_source(obj) -> bool:
+    return all(hasattr(obj, k) for k in ("n", "num_settings", "frequencies"))
+
+
+def _as_source(record_or_source):
+    """pipeline.py:54-59: records are validated, states become ExactFrequencies; an exact
+    source of a dyadic state is its noiseless integer record (identical estimate)."""
+    src = record_or_source
+    if isinstance(src, StateDescriptor):
+        src = ExactFrequencies(src)
+    if isinstance(src, ExactFrequencies) and src.state.dyadic:
+        return src.state  # to_device_record: exact_record on the device
+    if isinstance(src, (MeasurementRecord, DeviceRecord, OutcomeRecord)):
+        return src
+    if _is_frequency_source(src):
+        pauli.check_qubit_count(int(src.n))
+        if int(src.num_settings) != 3 ** int(src.n):
+            raise ValueError(f"source has {src.num_settings} settings, expected 3**{src.n}")
+        return src
+    raise TypeError(f"unsupported source {type(record_or_source).__name__}: pass a MeasurementRecord, DeviceRecord, "
+                    "OutcomeRecord, StateDescriptor or an object with .n, .num_settings and .frequencies(a, b)")
 
 def to_device_record(record_or_source, device=None, stream=None) -> DeviceRecord:
     """Resolve any supported source into a validated DeviceRecord (pipeline.py:54-59)."""
@@ -118,8 +163,9 @@ def to_device_record(record_or_source, device=None, stream=None) -> DeviceRecord
         rec._validated = True
         return drec
     raise TypeError(
-        f"unsupported source {type(record_or_source).__name__}: pass a MeasurementRecord, DeviceRecord "
-        "or StateDescriptor"
+        f"unsupported source {type(record_or_source).__name__}: pass a MeasurementRecord, DeviceRecord, "
+        "OutcomeRecord or a dyadic StateDescriptor (frequency sources go through reconstruct / "
+        "step_one_least_squares)"
     )
 
 
@@ -280,6 +326,127 @@ class LREPlan:
         self.step2(stream)
 
 
+class F64Plan:
+    """Step (i) from fp64 frequency sources (lre_step1_f64_*) plus step (ii).
+
+    The source is consumed in setting chunks (a multiple of lre_step1_f64_quantum):
+    exact sources of non-dyadic states have their probabilities evaluated on the
+    device chunk by chunk (lre_theta_probabilities); any other source's
+    ``frequencies(a, b)`` blocks are copied from the host through two pinned
+    buffers on a copy stream, overlapped with the folding of the previous chunk.
+    ``mu`` lives in the workspace (dead once theta is final), as in LREPlan."""
+
+    def __init__(self, n: int, device=None, chunk_bytes: int = 1 << 28, with_mu: bool = True):
+        import ctypes
+
+        torch = _torch()
+        self.n = pauli.check_qubit_count(n)
+        self.device = _device(device)
+        L = _lib.load()
+        q = int(L.lre_step1_f64_quantum(self.n))
+        settings, d = 3**self.n, 1 << self.n
+        rows = max(q, (max(1, chunk_bytes // (8 * d)) // q) * q)
+        self.chunk_rows = min(settings, rows)
+        ws, sc = ctypes.c_size_t(0), ctypes.c_size_t(0)
+        _lib.check(L.lre_step1_f64_workspace(self.n, self.chunk_rows, ctypes.byref(ws), ctypes.byref(sc)),
+                   "lre_step1_f64_workspace")
+        self.ws_bytes, self.scratch_bytes = int(ws.value), int(sc.value)
+        mu_bytes = 16 * d * d if with_mu else 0
+        self.ws = torch.empty(max(self.ws_bytes, mu_bytes, 256), dtype=torch.uint8, device=self.device)
+        self.scratch = torch.empty(max(self.scratch_bytes, 256), dtype=torch.uint8, device=self.device)
+        self.theta = torch.empty(4**self.n, dtype=torch.float64, device=self.device)
+        self.mu = self.ws[:mu_bytes].view(torch.complex128).view(d, d) if with_mu else None
+        self.layout = _lib.MASK_MAJOR if self.n >= 11 else _lib.NATURAL
+
+    def stage(self, freq, w_begin: int, w_end: int, stream) -> None:
+        torch = _torch()
+        rows = int(w_end) - int(w_begin)
+        if not isinstance(freq, torch.Tensor) or freq.dtype != torch.float64 or not freq.is_cuda \
+                or tuple(freq.shape) != (rows, 1 << self.n) or not freq.is_contiguous():
+            raise ValueError(f"frequency chunk must be a contiguous CUDA float64 tensor of shape {(rows, 1 << self.n)}")
+        _lib.call("lre_step1_f64_stage", freq.data_ptr(), self.n, int(w_begin), int(w_end), self.ws.data_ptr(),
+                  self.ws_bytes, self.scratch.data_ptr(), self.scratch_bytes, stream.cuda_stream)
+
+    def finish(self, stream) -> None:
+        _lib.call("lre_step1_f64_finish", self.ws.data_ptr(), self.ws_bytes, self.n, self.theta.data_ptr(),
+                  self.layout, stream.cuda_stream)
+
+    def step1(self, source, stream) -> None:
+        """Every chunk of `source` staged, then the remaining passes (theta final)."""
+        torch = _torch()
+        settings, d = 3**self.n, 1 << self.n
+        exact = isinstance(source, ExactFrequencies)
+        bufs = [torch.empty((self.chunk_rows, d), dtype=torch.float64, device=self.device) for _ in range(2)]
+        if exact:
+            theta_true = state_theta(source.state, self.device)
+            for k, lo in enumerate(range(0, settings, self.chunk_rows)):
+                hi = min(settings, lo + self.chunk_rows)
+                blk = bufs[k % 2][: hi - lo]
+                theta_probabilities(theta_true, self.n, lo, hi, clip=True, out=blk, stream=stream)
+                self.stage(blk, lo, hi, stream)
+        else:
+            copy = torch.cuda.Stream(self.device)
+            pinned = [torch.empty((self.chunk_rows, d), dtype=torch.float64, pin_memory=True) for _ in range(2)]
+            ev_copy = [torch.cuda.Event() for _ in range(2)]
+            ev_used = [torch.cuda.Event() for _ in range(2)]
+            for k, lo in enumerate(range(0, settings, self.chunk_rows)):
+                hi = min(settings, lo + self.chunk_rows)
+                b = k % 2
+                block = np.asarray(source.frequencies(lo, hi), dtype=np.float64)
+                if block.shape != (hi - lo, d):
+                    raise ValueError(f"frequencies({lo}, {hi}) returned shape {block.shape}, expected {(hi - lo, d)}")
+                ev_used[b].synchronize()  # the pinned buffer's previous H2D copy has been consumed
+                pinned[b][: hi - lo].numpy()[...] = block
+                copy.wait_event(ev_used[b])
+                with torch.cuda.stream(copy):
+                    bufs[b][: hi - lo].copy_(pinned[b][: hi - lo], non_blocking=True)
+                    ev_copy[b].record(copy)
+                stream.wait_event(ev_copy[b])
+                self.stage(bufs[b][: hi - lo], lo, hi, stream)
+                ev_used[b].record(stream)
+            torch.cuda.current_stream(self.device).wait_stream(copy)
+        self.finish(stream)
+
+    step2 = LREPlan.step2
+    export_buffer = LREPlan.export_buffer
+    theta_natural = LREPlan.theta_natural
+
+
+def _reconstruct_frequencies(source, stream, project: bool, device, workers, kernel, as_tensor):
+    """reconstruct() for fp64 frequency sources (F64Plan)."""
+    torch = _torch()
+    n = pauli.check_qubit_count(int(source.n))
+    if n > DENSE_PIPELINE_MAX_QUBITS:
+        raise ValueError(f"n={n} needs a dense {2**n}x{2**n} complex allocation; the dense pipeline is capped "
+                         f"at n={DENSE_PIPELINE_MAX_QUBITS}")
+    dev = _device(device)
+    stream = stream if stream is not None else torch.cuda.current_stream(dev)
+    plan = F64Plan(n, dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev[0].record(stream)
+    plan.step1(source, stream)
+    ev[1].record(stream)
+    plan.step2(stream)
+    ev[2].record(stream)
+    rho, evals = step_three_project(plan.mu) if project else (plan.mu, None)
+    ev[3].record(stream)
+    theta = plan.theta_natural(stream, out=plan.export_buffer())
+    ev[4].record(stream)
+    ev[4].synchronize()
+    t1, t2, t3 = (ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(3))
+    timings = {"t_step1_s": t1, "t_step2_s": t2, "t_step3_s": t3, "t_total_s": t1 + t2 + t3, "threads": workers,
+               "kernel": kernel, "gpus": 1, "t_theta_export_s": ev[3].elapsed_time(ev[4]) / 1e3,
+               "source": "exact (device)" if isinstance(source, ExactFrequencies) else "frequencies (host)"}
+    timings.update(roofline_timings(n, 8, t1 + t2))
+    mu = plan.mu
+    if not as_tensor:
+        same = rho is mu
+        theta, mu = theta.cpu().numpy(), mu.cpu().numpy()
+        rho = mu if same else rho.cpu().numpy()
+        evals = None if evals is None else evals.cpu().numpy()
+    return ReconstructionResult(theta=theta, mu=mu, rho=rho, eigenvalues=evals, timings=timings)
+
+
 # ---------------------------------------------------------------------------
 # reference entry points
 # ---------------------------------------------------------------------------
@@ -289,7 +456,13 @@ def step_one_least_squares(record_or_source, workers: int = 1, kernel: str = "b2
     """Least-squares Pauli coefficients theta (natural order), pipeline.py:116-138."""
     _check_kernel(kernel)
     torch = _torch()
-    rec = to_device_record(record_or_source, device)
+    src = _as_source(record_or_source)
+    if not isinstance(src, (MeasurementRecord, DeviceRecord, OutcomeRecord, StateDescriptor)):
+        plan = F64Plan(int(src.n), device, with_mu=False)
+        plan.layout = _lib.NATURAL
+        plan.step1(src, torch.cuda.current_stream(plan.device))
+        return plan.theta if as_tensor else plan.theta.cpu().numpy()
+    rec = to_device_record(src, device)
     n = pauli.check_qubit_count(rec.n)
     stream = torch.cuda.current_stream(rec.counts.device)
     theta = torch.empty(4**n, dtype=torch.float64, device=rec.counts.device)
@@ -403,7 +576,10 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
     """
     _check_kernel(kernel)
     torch = _torch()
-    rec = to_device_record(record_or_source, device)
+    src = _as_source(record_or_source)
+    if not isinstance(src, (MeasurementRecord, DeviceRecord, OutcomeRecord, StateDescriptor)):
+        return _reconstruct_frequencies(src, None, project, device, workers, kernel, as_tensor)
+    rec = to_device_record(src, device)
     n = pauli.check_qubit_count(rec.n)
     if rec.w_begin != 0 or rec.w_end != 3**n:
         raise ValueError(f"reconstruct needs the full setting range [0, {3**n}), got [{rec.w_begin}, {rec.w_end})")

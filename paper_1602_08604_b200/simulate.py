@@ -108,12 +108,16 @@ def density_matrix(state: StateDescriptor) -> np.ndarray:
     return np.outer(psi, psi.conj())
 
 
-def dense_to_theta(rho, device=None, stream=None):
-    """Pauli coefficients (NATURAL, fp64, on the device) of a dense Hermitian
-    2^n x 2^n matrix: lre_dense_to_theta, the inverse of step (ii)
-    (replaces simulate.py:114-138)."""
+def dense_to_theta(rho, hermitian_tol: float = 1e-10, *, device=None, stream=None, as_tensor=None):
+    """Pauli coefficients theta_i = Tr(rho Omega_i) (NATURAL order, fp64) of a dense
+    Hermitian 2^n x 2^n matrix, computed on the device by lre_dense_to_theta (the
+    inverse of step (ii)); replaces simulate.py:114-138 with its Hermiticity check and
+    message.  Returns numpy for numpy input (the reference's type), a CUDA tensor for
+    tensor input or as_tensor=True."""
     import torch
 
+    if as_tensor is None:
+        as_tensor = isinstance(rho, torch.Tensor)
     device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     r = rho if isinstance(rho, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(rho, dtype=np.complex128))
     r = r.to(device=device, dtype=torch.complex128).contiguous()
@@ -121,12 +125,83 @@ def dense_to_theta(rho, device=None, stream=None):
     n = d.bit_length() - 1
     if r.dim() != 2 or int(r.shape[1]) != d or (1 << n) != d:
         raise ValueError(f"expected a square 2**n x 2**n matrix, got {tuple(r.shape)}")
+    pauli.check_qubit_count(n)
     if n > DENSE_MAX_QUBITS:
         raise ValueError(f"dense matrix at n={n} exceeds the {DENSE_MAX_QUBITS}-qubit cap")
+    asym = float((r - r.conj().T).abs().max().item())
+    if asym > hermitian_tol:
+        raise ValueError(f"matrix is not Hermitian (max asymmetry {asym:.3e})")
     theta = torch.empty(4**n, dtype=torch.float64, device=device)
     stream = stream if stream is not None else torch.cuda.current_stream(device)
     _lib.call("lre_dense_to_theta", r.data_ptr(), n, theta.data_ptr(), stream.cuda_stream)
-    return theta
+    return theta if as_tensor else theta.cpu().numpy()
+
+
+NEGATIVE_PROBABILITY_TOL = 1e-8  # simulate.py:22
+PROBABILITY_SUM_TOL = 1e-8  # simulate.py:23
+
+
+def theta_probabilities(theta, n: int, start: int, stop: int, clip: bool, out=None, stream=None):
+    """Device (start..stop) x 2^n outcome probabilities of the state with Pauli
+    coefficients theta (device, NATURAL): lre_theta_probabilities."""
+    import torch
+
+    if out is None:
+        out = torch.empty((stop - start, 1 << n), dtype=torch.float64, device=theta.device)
+    if stop > start:
+        stream = stream if stream is not None else torch.cuda.current_stream(theta.device)
+        _lib.call("lre_theta_probabilities", theta.data_ptr(), n, int(start), int(stop), 1 if clip else 0,
+                  out.data_ptr(), stream.cuda_stream)
+    return out
+
+
+def _check_probabilities(p, what):
+    """simulate.py:154-159, same messages."""
+    if p.min() < -NEGATIVE_PROBABILITY_TOL:
+        raise ValueError(f"{what}: negative probability {p.min():.3e}")
+    total = p.sum()
+    if abs(total - 1.0) > PROBABILITY_SUM_TOL:
+        raise ValueError(f"{what}: probabilities sum to {total!r}, not 1")
+
+
+def theta_to_probabilities(theta, w: int, n: int) -> np.ndarray:
+    """Outcome distribution of setting w for a state given as theta (simulate.py:141-145)."""
+    import torch
+
+    t = theta if isinstance(theta, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(theta, dtype=np.float64))
+    t = t.to(device=torch.device("cuda", torch.cuda.current_device()) if not t.is_cuda else t.device,
+             dtype=torch.float64).contiguous()
+    p = theta_probabilities(t, n, w, w + 1, clip=False)[0].cpu().numpy()
+    _check_probabilities(p, f"setting {pauli.setting_label(w, n)}")
+    return p
+
+
+def probabilities_block(state: StateDescriptor, start: int, stop: int, as_tensor: bool = False):
+    """Exact outcome probabilities of settings [start, stop) (simulate.py:167-206), on the
+    device: dyadic states (maxmixed, ghz, productz) as their noiseless record / 2^n, any
+    other state through its Pauli coefficients, clipped to [0, 1] (n <= 12)."""
+    import torch
+
+    n = state.n
+    if not 0 <= start <= stop <= 3**n:
+        raise ValueError(f"setting range [{start}, {stop}) out of bounds for n={n}")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    if state.dyadic:
+        counts = generate_device_counts(state, 1 << n, exact=True, w_begin=start, w_end=stop, device=dev)
+        p = counts.to(torch.float64) / float(1 << n)
+    else:
+        if n > DENSE_MAX_QUBITS:
+            raise ValueError(f"exact probabilities of {state.label()} need its dense matrix; capped at "
+                             f"n={DENSE_MAX_QUBITS}")
+        p = theta_probabilities(state_theta(state, dev), n, start, stop, clip=True)
+    return p if as_tensor else p.cpu().numpy()
+
+
+def exact_probabilities(state: StateDescriptor, w: int) -> np.ndarray:
+    """Exact outcome distribution of one setting (simulate.py:209-213)."""
+    if not 0 <= w < 3**state.n:
+        raise ValueError(f"setting index {w} out of range for n={state.n}")
+    return probabilities_block(state, w, w + 1)[0]
 
 
 _THETA_CACHE: dict = {}
@@ -140,7 +215,7 @@ def state_theta(state: StateDescriptor, device=None):
     key = (state, str(device))
     if key not in _THETA_CACHE:
         _THETA_CACHE.clear()  # one state at a time: theta is 8 * 4^n bytes
-        _THETA_CACHE[key] = dense_to_theta(density_matrix(state), device=device)
+        _THETA_CACHE[key] = dense_to_theta(density_matrix(state), device=device, as_tensor=True)
     return _THETA_CACHE[key]
 
 
@@ -166,7 +241,7 @@ def sample_counts_from_density(rho, shots: int, seed: int, dtype=None, device=No
     """Sampled record of an arbitrary dense state (n <= 12), drawn on the device."""
     if shots < 1:
         raise ValueError(f"shots must be >= 1, got {shots}")
-    theta = dense_to_theta(rho, device=device)
+    theta = dense_to_theta(rho, device=device, as_tensor=True)
     n = (int(theta.shape[0]).bit_length() - 1) // 2
     counts = generate_counts_from_theta(theta, n, shots, seed, dtype=dtype)
     return DeviceRecord(n=n, shots=shots, counts=counts, seed=seed, state="dense")
@@ -260,3 +335,6 @@ def sample_outcomes(state: StateDescriptor, shots: int, seed: int, device=None):
         raise ValueError(f"shots must be >= 1, got {shots}")
     outcomes = generate_device_outcomes(state, shots, seed=seed, device=device)
     return OutcomeRecord(n=state.n, shots=shots, outcomes=outcomes, seed=seed, state=state.label())
+
+
+dense_matrix = density_matrix  # the reference's name (simulate.py:86)

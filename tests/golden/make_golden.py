@@ -281,8 +281,29 @@ def metrics_cases():
           fids=np.array(json.dumps(fids)), **out)
 
 
+def exact_sources():
+    """reconstruct() on ExactFrequencies sources (pipeline.py:42-59,224-249): the reference's
+    own timing flow (bench.median_step_times) — random states n = 2..5 (non-dyadic, fp64
+    frequencies), ghz and maxmixed at n = 3 (dyadic), and a plain duck-typed source."""
+    cases = {}
+    for kind, n, seed in [("random", 2, 11), ("random", 4, 0), ("random", 5, 7), ("ghz", 3, 0), ("maxmixed", 3, 0)]:
+        st = simulate.StateDescriptor(kind, n, state_seed=seed)
+        res = pipeline.reconstruct(pipeline.ExactFrequencies(st), workers=1)
+        tag = f"{kind}{n}_{seed}"
+        cases.update({f"{tag}_theta": res.theta, f"{tag}_mu": res.mu, f"{tag}_rho": res.rho,
+                      f"{tag}_eigenvalues": res.eigenvalues,
+                      f"{tag}_probs": simulate.probabilities_block(st, 0, 3**n)})
+    # theta_to_probabilities / exact_probabilities on single settings
+    st = simulate.StateDescriptor("random", 3, state_seed=5)
+    theta = simulate.dense_to_theta(simulate.dense_matrix(st).astype(np.complex128))
+    cases["random3_5_dense_theta"] = theta
+    cases["random3_5_p_w7"] = simulate.theta_to_probabilities(theta, 7, 3)
+    cases["ghz3_p_w5"] = simulate.exact_probabilities(simulate.StateDescriptor("ghz", 3), 5)
+    _save("exact_sources.npz", **cases)
+
+
 if __name__ == "__main__":
-    todo = sys.argv[1:] or ["kat", "blocks", "c1", "small", "validate_messages", "c2", "c3", "files",
+    todo = sys.argv[1:] or ["kat", "blocks", "c1", "small", "validate_messages", "c2", "c3", "files", "exact_sources",
                             "metrics_cases"]
     for name in todo:
         globals()[name]()
