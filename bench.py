@@ -818,6 +818,11 @@ def run_dist(args, rank: int, world: int, local: int):
                            "frac_of_world_peak": b / t_step / 1e9 / (peak * world)},
             "cpu_baseline": None,
             "e2e": e2e,
+            "exchange": {"collective": "reduce_scatter_tensor (NCCL), int64 numerators",
+                         "chunks": comp.K, "nccl_bytes_per_rank": runner.nccl_bytes,
+                         "overlap": "chunk k finalised + assembled (lre_finalize, lre_assemble_slab) while chunk k+1 "
+                                    "transfers on a side stream" if comp.K > 1 else "none (one chunk)",
+                         "measured_on_hardware": world > 1},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }))

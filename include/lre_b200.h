@@ -41,6 +41,15 @@ typedef enum { LRE_U8 = 1, LRE_U16 = 2, LRE_I32 = 3, LRE_I64 = 4 } lre_dtype;
 
 typedef enum { LRE_LAYOUT_NATURAL = 0, LRE_LAYOUT_MASK_MAJOR = 1 } lre_layout;
 
+/*
+ * MASK_MAJOR with the X-masks permuted for a chunked exchange over P = 2^logP
+ * ranks in K = 2^logK chunks (step (i) outputs only): mask m = (g, c, j), g =
+ * m / S (S = 2^n / P), c = (m % S) / (S / K), j = m % (S / K), is stored at
+ * mask position (c * P + g) * (S / K) + j, so chunk c of every rank's slice is
+ * one contiguous P x (S/K) x 2^n block: reduce-scatter chunk c.
+ */
+#define LRE_LAYOUT_MASK_CHUNKED(logP, logK) (2 | ((logP) << 8) | ((logK) << 16))
+
 typedef enum {
     LRE_OUT_THETA_F64 = 0, /* finished theta (fp64), requires the full setting range */
     LRE_OUT_NUM_I64 = 1    /* exact int64 numerators N_i (partial sums allowed)     */
@@ -160,6 +169,17 @@ int lre_theta_relayout(const double *src, int src_layout, int n, double *dst, lr
  */
 int lre_assemble(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu_out,
                  lre_stream_t stream);
+
+/*
+ * One chunk of a rank's step (ii): masks [m_begin, m_end) (theta: their
+ * mask-major slice) written into the column slab of the masks [slab_begin,
+ * slab_begin + slab_masks) laid out as lre_assemble's output for that range:
+ *   mu_slab[r*slab_masks + c] = mu[r, ((r / slab_masks) ^ (slab_begin / slab_masks))*slab_masks + c].
+ * m_end - m_begin a power of two dividing m_begin; chunks smaller than the slab
+ * need n >= 11 and >= 8 masks (LRE_EUNSUPPORTED otherwise).
+ */
+int lre_assemble_slab(const double *theta, int n, int64_t m_begin, int64_t m_end, int64_t slab_begin,
+                      int64_t slab_masks, double *mu_slab, lre_stream_t stream);
 
 /*
  * Record validation (reference records.py:34-56, MeasurementRecord.validate):

@@ -18,6 +18,11 @@ LIB_PATH = os.environ.get("LRE_LIB_PATH") or os.path.join(_HERE, "_lib", "liblre
 LRE_OK, LRE_EINVAL, LRE_ECUDA, LRE_ENOMEM, LRE_EUNSUPPORTED, LRE_EOVERFLOW = range(6)
 U8, U16, I32, I64 = 1, 2, 3, 4
 NATURAL, MASK_MAJOR = 0, 1
+
+
+def MASK_CHUNKED(log_p: int, log_k: int) -> int:
+    """LRE_LAYOUT_MASK_CHUNKED(logP, logK) of include/lre_b200.h."""
+    return 2 | (log_p << 8) | (log_k << 16)
 OUT_THETA_F64, OUT_NUM_I64 = 0, 1
 STATE_KINDS = {"maxmixed": 0, "ghz": 1, "productz": 2, "w": 3}
 REDUCE_BLOCKS = 1184  # LRE_REDUCE_BLOCKS
@@ -43,6 +48,7 @@ _SIGNATURES = {
     "lre_finalize": (_i, [_vp, _i, _i64, _i, _i64, _i64, _vp, _vp]),
     "lre_theta_relayout": (_i, [_vp, _i, _i, _vp, _vp]),
     "lre_assemble": (_i, [_vp, _i, _i, _i64, _i64, _vp, _vp]),
+    "lre_assemble_slab": (_i, [_vp, _i, _i64, _i64, _i64, _i64, _vp, _vp]),
     "lre_validate_counts": (_i, [_vp, _i, _i, _i64, _i64, _vp, _vp]),
     "lre_generate_counts": (_i, [_i, _i, _i64, _i64, _u64, _i, _i64, _i64, _vp, _i, _vp]),
     "lre_generate_outcomes": (_i, [_i, _i, _i64, _i64, _u64, _i64, _i64, _vp, _vp]),

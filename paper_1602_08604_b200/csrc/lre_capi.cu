@@ -41,6 +41,8 @@ int theta_probabilities_impl(const double *theta, int n, int64_t w_begin, int64_
                              cudaStream_t s);
 int64_t shard_quantum(int n, int64_t shots);
 int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s);
+int assemble_slab_impl(const double *theta, int n, int64_t m_begin, int64_t m_end, int64_t slab_begin,
+                       int64_t slab_masks, double *mu, cudaStream_t s);
 int validate_impl(const void *counts, int dtype, int n, int64_t rows, int64_t shots, int64_t *result,
                   cudaStream_t s);
 int finalize_impl(const int64_t *num, int n, int64_t shots, int layout, int64_t begin, int64_t end, double *theta,
@@ -77,6 +79,14 @@ static inline int64_t dtype_max(int dtype) {
 
 static inline bool valid_n(int n) { return n >= 1 && n <= 16; }
 
+// NATURAL, MASK_MAJOR, or MASK_CHUNKED(logP, logK) with 2^(logP+logK) <= 2^n masks
+static inline bool valid_layout(int layout, int n) {
+    if (layout == LRE_LAYOUT_NATURAL || layout == LRE_LAYOUT_MASK_MAJOR) return true;
+    if ((layout & 0xff) != 2 || (layout >> 24)) return false;
+    const int logP = (layout >> 8) & 0xff, logK = (layout >> 16) & 0xff;
+    return logP + logK <= n;
+}
+
 extern "C" {
 
 const char *lre_strerror(int status) {
@@ -111,7 +121,7 @@ int lre_step1(const void *counts, int count_dtype, int n, int64_t shots, int64_t
     if (shots > dtype_max(count_dtype) && count_dtype != LRE_I64) return LRE_EOVERFLOW;
     if (w_begin < 0 || w_end > pow3_i(n) || w_begin >= w_end) return LRE_EINVAL;
     if (out_kind != LRE_OUT_THETA_F64 && out_kind != LRE_OUT_NUM_I64) return LRE_EINVAL;
-    if (layout != LRE_LAYOUT_NATURAL && layout != LRE_LAYOUT_MASK_MAJOR) return LRE_EINVAL;
+    if (!valid_layout(layout, n)) return LRE_EINVAL;
     if (out_kind == LRE_OUT_THETA_F64 && (w_begin != 0 || w_end != pow3_i(n))) return LRE_EINVAL;
     const int64_t q = lre::shard_quantum(n, shots);
     if (w_begin % q || (w_end % q && w_end != pow3_i(n))) return LRE_EINVAL;
@@ -140,7 +150,7 @@ int lre_step1_finish(void *workspace, size_t workspace_bytes, int n, int64_t sho
                      int layout, lre_stream_t stream) {
     if (!valid_n(n) || !out || shots < 1) return LRE_EINVAL;
     if (out_kind != LRE_OUT_THETA_F64 && out_kind != LRE_OUT_NUM_I64) return LRE_EINVAL;
-    if (layout != LRE_LAYOUT_NATURAL && layout != LRE_LAYOUT_MASK_MAJOR) return LRE_EINVAL;
+    if (!valid_layout(layout, n)) return LRE_EINVAL;
     return lre::step1_finish_impl(workspace, workspace_bytes, n, shots, out, out_kind, layout,
                                   reinterpret_cast<cudaStream_t>(stream));
 }
@@ -194,6 +204,13 @@ int lre_assemble(const double *theta, int layout, int n, int64_t m_begin, int64_
     if (!valid_n(n) || !theta || !mu_out) return LRE_EINVAL;
     if (layout != LRE_LAYOUT_NATURAL && layout != LRE_LAYOUT_MASK_MAJOR) return LRE_EINVAL;
     return lre::assemble_impl(theta, layout, n, m_begin, m_end, mu_out, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int lre_assemble_slab(const double *theta, int n, int64_t m_begin, int64_t m_end, int64_t slab_begin,
+                      int64_t slab_masks, double *mu_slab, lre_stream_t stream) {
+    if (!valid_n(n) || !theta || !mu_slab) return LRE_EINVAL;
+    return lre::assemble_slab_impl(theta, n, m_begin, m_end, slab_begin, slab_masks, mu_slab,
+                                   reinterpret_cast<cudaStream_t>(stream));
 }
 
 int lre_validate_counts(const void *counts, int count_dtype, int n, int64_t rows, int64_t shots, int64_t *result,

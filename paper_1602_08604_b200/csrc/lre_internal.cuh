@@ -217,6 +217,21 @@ __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+// Mask position of X-mask m in a MASK_MAJOR-family layout (include/lre_b200.h):
+// plain MASK_MAJOR is the identity; MASK_CHUNKED(logP, logK) swaps the rank field
+// g (top logP bits of m) with the chunk field c (next logK bits), so that chunk c
+// of every rank's mask slice is one contiguous block (a reduce-scatter chunk).
+__host__ __device__ __forceinline__ uint64_t mask_position(uint64_t m, int n, int layout) {
+    if ((layout & 0xff) != 2) return m;
+    const int logP = (layout >> 8) & 0xff, logK = (layout >> 16) & 0xff;
+    const int logS = n - logP, logJ = logS - logK;
+    const uint64_t g = m >> logS, c = (m >> logJ) & ((1ull << logK) - 1), j = m & ((1ull << logJ) - 1);
+    return (((c << logP) | g) << logJ) | j;
+}
+__host__ __device__ __forceinline__ bool layout_is_mask_major(int layout) {
+    return layout == LRE_LAYOUT_MASK_MAJOR || (layout & 0xff) == 2;
+}
+
 // 3^k as an exact double (k <= 32)
 __device__ __forceinline__ double pow3d(int k) {
     double g = 1.0;

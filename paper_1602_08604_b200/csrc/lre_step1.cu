@@ -54,10 +54,10 @@ struct Final {
 // store a finished fp64 numerator (frequency sources: theta = N * fac[zc], fac from shots = 1)
 __device__ __forceinline__ void store_final(const Final &f, const double *sfac, uint64_t nat, double v) {
     uint64_t pos = nat;
-    if (f.layout == LRE_LAYOUT_MASK_MAJOR) {
+    if (layout_is_mask_major(f.layout)) {
         uint32_t m, a;
         natural_to_ma(nat, m, a);
-        pos = ((uint64_t)m << f.n) | a;
+        pos = (mask_position(m, f.n, f.layout) << f.n) | a;
     }
     const int zc = f.n - __popcll((nat | (nat >> 1)) & 0x5555555555555555ull);
     reinterpret_cast<double *>(f.out)[pos] = v * sfac[zc];
@@ -66,10 +66,10 @@ __device__ __forceinline__ void store_final(const Final &f, const double *sfac, 
 // store a finished numerator at natural Pauli index `nat`; sfac = the staged fac table
 __device__ __forceinline__ void store_final(const Final &f, const double *sfac, uint64_t nat, int64_t v) {
     uint64_t pos = nat;
-    if (f.layout == LRE_LAYOUT_MASK_MAJOR) {
+    if (layout_is_mask_major(f.layout)) {
         uint32_t m, a;
         natural_to_ma(nat, m, a);
-        pos = ((uint64_t)m << f.n) | a;
+        pos = (mask_position(m, f.n, f.layout) << f.n) | a;
     }
     if (f.kind == OUT_NUM) {
         reinterpret_cast<int64_t *>(f.out)[pos] = v;
@@ -1545,7 +1545,7 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
             const uint64_t m = (mt << (n - 1)) | ((uint64_t)mh << 5) | (uint64_t)m5;
             const uint64_t aa = (at << (n - 1)) | ((uint64_t)ah << 5) | (uint64_t)lane;
             const double val = st[row * 33 + lane];
-            const uint64_t pos = (m << n) | aa;
+            const uint64_t pos = (mask_position(m, n, a.f.layout) << n) | aa;
             if constexpr (NUM) reinterpret_cast<int64_t *>(a.f.out)[pos] = (int64_t)__double_as_longlong(val);
             else __stcs(reinterpret_cast<double *>(a.f.out) + pos, val);
         }
@@ -1662,7 +1662,7 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             }();
             a.vf1_batch = vf1;
             a.f = f;
-            const bool fmm = fin && ps.q == 1 && layout == LRE_LAYOUT_MASK_MAJOR && a.V >= 1024 && a.A0 == 0 && a.nA == 1 &&
+            const bool fmm = fin && ps.q == 1 && layout_is_mask_major(layout) && a.V >= 1024 && a.A0 == 0 && a.nA == 1 &&
                              a.nB == 1 && (ps.in_dtype == LRE_I32 || ps.in_dtype == LRE_I64);
             e = fmm ? launch_final_mm(ps.in_dtype, ps.acc64, a, stream) : run_vfold(ps.q, ps.in_dtype, ps.acc64, a, stream);
         }

@@ -347,8 +347,8 @@ __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.w
 struct X8Args {
     const double *theta;  // mask-major slice: theta[(m - m_begin) * 2^n + a]
     int64_t m_begin;
-    int64_t S;            // masks in the slice (power of two >= 8); mu rows are S complex wide
-    int64_t units;        // S / 8
+    int64_t S;            // mu rows are S complex wide: the slab of S masks holding [m_begin, m_begin + 8 units)
+    int64_t units;        // masks / 8
     double scale_half;
     double2 *mu;
 };
@@ -692,7 +692,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
 }
 
 template <int LOGD>
-static int launch_x8(const double *theta, int64_t m_begin, int64_t S, double *mu, cudaStream_t s) {
+static int launch_x8(const double *theta, int64_t m_begin, int64_t masks, int64_t S, double *mu, cudaStream_t s) {
     using C = X8<LOGD>;
     auto kern = assemble_x8_kernel<LOGD>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
@@ -701,7 +701,7 @@ static int launch_x8(const double *theta, int64_t m_begin, int64_t S, double *mu
     a.theta = theta;
     a.m_begin = m_begin;
     a.S = S;
-    a.units = S / 8;
+    a.units = masks / 8;
     a.scale_half = 0.5 * pow(2.0, -LOGD / 2.0);
     a.mu = reinterpret_cast<double2 *>(mu);
     cudaLaunchConfig_t cfg = {};
@@ -736,14 +736,35 @@ static bool use_cl8(int layout, int n, int64_t S) {
     return !legacy && layout == LRE_LAYOUT_MASK_MAJOR && n >= 11 && n <= 14 && S >= 8;
 }
 
-static int launch_cl8_n(int n, const double *theta, int64_t m_begin, int64_t S, double *mu, cudaStream_t s) {
+static int launch_cl8_n(int n, const double *theta, int64_t m_begin, int64_t masks, int64_t S, double *mu,
+                        cudaStream_t s) {
     switch (n) {
-    case 11: return launch_x8<11>(theta, m_begin, S, mu, s);
-    case 12: return launch_x8<12>(theta, m_begin, S, mu, s);
-    case 13: return launch_x8<13>(theta, m_begin, S, mu, s);
-    case 14: return launch_x8<14>(theta, m_begin, S, mu, s);
+    case 11: return launch_x8<11>(theta, m_begin, masks, S, mu, s);
+    case 12: return launch_x8<12>(theta, m_begin, masks, S, mu, s);
+    case 13: return launch_x8<13>(theta, m_begin, masks, S, mu, s);
+    case 14: return launch_x8<14>(theta, m_begin, masks, S, mu, s);
     default: return LRE_EUNSUPPORTED;
     }
+}
+
+int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s);
+
+// masks [m_begin, m_end) (mask-major slice) written into the column slab of the
+// masks [slab_begin, slab_begin + slab_masks): mu_slab[r * slab_masks + c] =
+// mu[r, ((r / slab_masks) ^ (slab_begin / slab_masks)) * slab_masks + c] —
+// one chunk of a rank's slice assembled as soon as its reduce-scatter chunk lands
+int assemble_slab_impl(const double *theta, int n, int64_t m_begin, int64_t m_end, int64_t slab_begin,
+                       int64_t slab_masks, double *mu, cudaStream_t s) {
+    const int64_t masks = m_end - m_begin;
+    const int64_t d = (int64_t)1 << n;
+    if (slab_masks <= 0 || (slab_masks & (slab_masks - 1)) || slab_begin % slab_masks || slab_begin + slab_masks > d)
+        return LRE_EINVAL;
+    if (masks <= 0 || (masks & (masks - 1)) || m_begin % masks || m_begin < slab_begin ||
+        m_end > slab_begin + slab_masks)
+        return LRE_EINVAL;
+    if (masks == slab_masks) return assemble_impl(theta, LRE_LAYOUT_MASK_MAJOR, n, m_begin, m_end, mu, s);
+    if (!use_cl8(LRE_LAYOUT_MASK_MAJOR, n, masks)) return LRE_EUNSUPPORTED;
+    return launch_cl8_n(n, theta, m_begin, masks, slab_masks, mu, s);
 }
 
 int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64_t m_end, double *mu, cudaStream_t s) {
@@ -751,7 +772,7 @@ int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64
     const int64_t d = (int64_t)1 << n;
     if (n < 1 || n > 14) return LRE_EUNSUPPORTED;
     if (S <= 0 || (S & (S - 1)) || m_begin % S || m_end > d) return LRE_EINVAL;
-    if (use_cl8(layout, n, S)) return launch_cl8_n(n, theta, m_begin, S, mu, s);
+    if (use_cl8(layout, n, S)) return launch_cl8_n(n, theta, m_begin, S, S, mu, s);
     const int Dp = (int)(d + (d >> 4) + 1);
     // shared-memory budget per CTA (masks per CTA = largest power of two that
     // fits): measured best 40 KB at n <= 11 (several CTAs per SM), 75 KB at

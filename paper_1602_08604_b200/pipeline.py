@@ -567,16 +567,23 @@ class ReconstructionResult:
 
 
 def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, device=None, project: bool = True,
-                as_tensor: bool = False) -> ReconstructionResult:
+                as_tensor: bool = False, devices=None) -> ReconstructionResult:
     """All three steps with per-step device timings (pipeline.py:224-249).
 
     Validation happens before the timer, as in the reference.  ``timings``
     has the reference keys t_step1_s / t_step2_s / t_step3_s / t_total_s /
-    threads / kernel, measured with CUDA events, plus gpus.
+    threads / kernel, measured with CUDA events, plus gpus and the SURVEY §5
+    keys bytes / gbps / roofline_frac.  ``devices`` (an int P or a list of
+    devices, P a power of two) shards an integer record's settings over P GPUs of
+    this process and exchanges the partial numerators peer to peer
+    (distributed.LocalShardedLRE); the estimate is bit-identical
+    to the one-GPU path.
     """
     _check_kernel(kernel)
     torch = _torch()
     src = _as_source(record_or_source)
+    if devices is not None and not (isinstance(devices, int) and devices == 1 and device is None):
+        return _reconstruct_devices(src, devices, project, workers, kernel, as_tensor)
     if not isinstance(src, (MeasurementRecord, DeviceRecord, OutcomeRecord, StateDescriptor)):
         return _reconstruct_frequencies(src, None, project, device, workers, kernel, as_tensor)
     rec = to_device_record(src, device)
@@ -629,6 +636,63 @@ def reconstruct(record_or_source, workers: int = 1, kernel: str = "b200", *, dev
     }
     timings.update(roofline_timings(n, rec.counts.element_size(), t1 + t2))
     mu = plan.mu
+    if not as_tensor:
+        same = rho is mu
+        theta, mu = theta.cpu().numpy(), mu.cpu().numpy()
+        rho = mu if same else rho.cpu().numpy()
+        evals = None if evals is None else evals.cpu().numpy()
+    return ReconstructionResult(theta=theta, mu=mu, rho=rho, eigenvalues=evals, timings=timings)
+
+
+def _reconstruct_devices(src, devices, project: bool, workers, kernel, as_tensor):
+    """reconstruct(..., devices=P): settings sharded over P devices of this process."""
+    torch = _torch()
+    from . import distributed as D
+
+    if isinstance(devices, int):
+        devs = [torch.device("cuda", i) for i in range(devices)]
+    else:
+        devs = [_device(x) for x in devices]
+    P = len(devs)
+    if isinstance(src, StateDescriptor):
+        src = exact_record(src, device=devs[0])
+    if not isinstance(src, (MeasurementRecord, DeviceRecord, OutcomeRecord)):
+        raise ValueError("devices= shards integer records (MeasurementRecord, DeviceRecord, OutcomeRecord, dyadic "
+                         "exact states); reconstruct frequency sources on one device")
+    rec = to_device_record(src, devs[0])
+    n = pauli.check_qubit_count(rec.n)
+    if rec.w_begin != 0 or rec.w_end != 3**n:
+        raise ValueError(f"reconstruct needs the full setting range [0, {3**n}), got [{rec.w_begin}, {rec.w_end})")
+    D.mask_range(n, P, 0)  # P must be a power of two <= 2^n
+    q = int(_lib.load().lre_shard_quantum(n))
+    ranges = D.shard_ranges(n, P, q)
+    comps = [D.DeviceCompute(n, rec.shots, lo, hi, P, g, devs[g]) for g, (lo, hi) in enumerate(ranges)]
+    shards = [rec.counts[lo:hi] if devs[g] == rec.counts.device else rec.counts[lo:hi].to(devs[g])
+              for g, (lo, hi) in enumerate(ranges)]
+    for dv in devs:
+        torch.cuda.synchronize(dv)
+    runner = D.LocalShardedLRE(comps)
+    stream = torch.cuda.current_stream(devs[0])
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record(stream)
+    runner.step(shards, rec.lre_dtype)
+    for dv in devs[1:]:
+        torch.cuda.current_stream(devs[0]).wait_stream(torch.cuda.current_stream(dv))
+    ev[1].record(stream)
+    mu = runner.gather()
+    theta_mm = runner.theta_mask_major()
+    ev[2].record(stream)
+    rho, evals = step_three_project(mu) if project else (mu, None)
+    ev[3].record(stream)
+    theta = torch.empty_like(theta_mm)
+    _lib.call("lre_theta_relayout", theta_mm.data_ptr(), _lib.MASK_MAJOR, n, theta.data_ptr(), stream.cuda_stream)
+    ev[3].synchronize()
+    t12 = ev[0].elapsed_time(ev[1]) / 1e3
+    t3 = ev[2].elapsed_time(ev[3]) / 1e3
+    timings = {"t_step12_s": t12, "t_gather_s": ev[1].elapsed_time(ev[2]) / 1e3, "t_step3_s": t3,
+               "t_total_s": t12 + t3, "threads": workers, "kernel": kernel, "gpus": P,
+               "exchange_chunks": comps[0].K}
+    timings.update(roofline_timings(n, rec.counts.element_size(), t12))
     if not as_tensor:
         same = rho is mu
         theta, mu = theta.cpu().numpy(), mu.cpu().numpy()

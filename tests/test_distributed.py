@@ -45,40 +45,55 @@ def test_mask_range_partition():
 
 
 class OracleCompute:
-    """CPU stand-in for DeviceCompute (same attributes and calls)."""
+    """CPU stand-in for DeviceCompute (same attributes and calls, incl. the chunked exchange)."""
 
-    def __init__(self, n, shots, w_lo, w_hi, world, rank):
+    def __init__(self, n, shots, w_lo, w_hi, world, rank, chunks=1):
         self.n, self.shots, self.w_lo, self.w_hi = n, shots, w_lo, w_hi
+        self.world, self.rank, self.K = world, rank, chunks
         d = 1 << n
         self.m_lo, self.m_hi = D.mask_range(n, world, rank)
         S = self.m_hi - self.m_lo
         m, a = O.symplectic_index(n)
-        self.pos = (m << n) | a  # natural index -> mask-major position
+        log_p, log_k = world.bit_length() - 1, chunks.bit_length() - 1
+        mp_ = np.array([D.mask_position(int(x), n, log_p, log_k) for x in range(d)], dtype=np.int64)
+        self.pos = (mp_[m] << n) | a  # natural index -> (chunked) mask-major position
+        self.chunk_elems = (S // chunks) * d
         self.recv = torch.empty(S * d, dtype=torch.int64)
+        self.mu = np.empty((d, S), dtype=np.complex128)
 
     def partial_numerators(self, counts, count_dtype):
         nat = C.numerators(counts, self.n, self.w_lo)
         mm = np.empty_like(nat)
         mm[self.pos] = nat
-        return torch.from_numpy(mm)
+        self.num = torch.from_numpy(mm)
+        return self.num
 
-    def finalize_and_assemble(self):
+    def chunk_in(self, c):
+        e = self.chunk_elems * self.world
+        return self.num[c * e:(c + 1) * e]
+
+    def chunk_out(self, c):
+        return self.recv[c * self.chunk_elems:(c + 1) * self.chunk_elems]
+
+    def finalize_assemble_chunk(self, c):
         n, d = self.n, 1 << self.n
-        mm = np.zeros(4**n, dtype=np.int64)
-        mm[self.m_lo * d:self.m_hi * d] = self.recv.numpy()
-        theta = O.finalize_numerators(mm[self.pos], n, self.shots)  # natural, zeros outside owned masks
         S = self.m_hi - self.m_lo
-        diag = C.step_two_masks(theta, n, self.m_lo, self.m_hi)    # (S, d): mu[r, r^m]
-        mu = np.empty((d, S), dtype=np.complex128)
+        sk = S // self.K
+        m0 = self.m_lo + c * sk
+        # the chunk's numerators: masks [m0, m0 + sk), mask-major
+        full = np.zeros(4**n, dtype=np.int64)
+        full[m0 * d:(m0 + sk) * d] = self.chunk_out(c).numpy()
+        m, a = O.symplectic_index(n)
+        theta = O.finalize_numerators(full[(m << n) | a], n, self.shots)  # natural, zeros outside the chunk
+        diag = C.step_two_masks(theta, n, m0, m0 + sk)  # (sk, d): mu[r, r^m]
         rows = np.arange(d)
         g = self.m_lo // S
-        for j in range(S):
-            m = self.m_lo + j
-            cols = rows ^ m
+        for j in range(sk):
+            cols = rows ^ (m0 + j)
             # slab layout of lre_assemble: mu_out[r, c] = mu[r, ((r // S) ^ g) * S + c]
             assert np.all(cols // S == (rows // S) ^ g)
-            mu[rows, cols % S] = diag[j]
-        return mu
+            self.mu[rows, cols % S] = diag[j]
+        return self.mu
 
 
 def _free_port():
@@ -87,29 +102,54 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, shots, counts, out_path):
+def _worker(rank, world, port, n, shots, counts, out_path, chunks=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lo, hi = D.shard_ranges(n, world, 3 ** min(n, 7))[rank]
-    comp = OracleCompute(n, shots, lo, hi, world, rank)
+    comp = OracleCompute(n, shots, lo, hi, world, rank, chunks)
     mu = D.ShardedLRE(comp).step(counts[lo:hi], None)
     np.save(f"{out_path}.{rank}.npy", mu)
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n", [7, 8])
-def test_world2_gloo_matches_single_rank(tmp_path, rng, n):
+@pytest.mark.parametrize("n,world,chunks", [(7, 2, 1), (8, 2, 1), (8, 2, 4), (8, 4, 1), (8, 4, 2)])
+def test_gloo_exchange_matches_single_rank(tmp_path, rng, n, world, chunks):
+    """world 2 and 4, whole-slice and chunked (MASK_CHUNKED layout) reduce-scatters."""
     shots = 300
     counts = random_counts(rng, n, shots, np.uint16)
-    world = 2
     out = str(tmp_path / "mu")
-    mp.spawn(_worker, args=(world, _free_port(), n, shots, counts, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), n, shots, counts, out, chunks), nprocs=world, join=True)
     theta = C.step_one(counts, n, shots)
     full = C.step_two(theta, n)
     d, S = 1 << n, (1 << n) // world
     for g in range(world):
         slab = np.load(f"{out}.{g}.npy")
         for r in range(0, d, 7):
+            cols = ((r // S) ^ g) * S + np.arange(S)
+            np.testing.assert_allclose(slab[r], full[r, cols], rtol=1e-12, atol=1e-15)
+
+
+def test_mask_chunked_layout_is_a_permutation():
+    for n, lp, lk in [(4, 1, 1), (8, 2, 2), (8, 3, 0), (10, 0, 2)]:
+        pos = [D.mask_position(m, n, lp, lk) for m in range(1 << n)]
+        assert sorted(pos) == list(range(1 << n))
+        S, K = (1 << n) >> lp, 1 << lk
+        for m in range(1 << n):  # chunk c of rank g lands in block c, sub-block g
+            g, c, j = m // S, (m % S) // (S // K), m % (S // K)
+            assert pos[m] == (c * (1 << lp) + g) * (S // K) + j
+
+
+def test_local_multi_device_exchange_matches_single(rng):
+    """LocalShardedLRE (one process, P 'devices') with oracle compute objects, chunked."""
+    n, shots, P = 8, 200, 4
+    counts = random_counts(rng, n, shots, np.uint16)
+    q = 3 ** min(n, 7)
+    cs = [OracleCompute(n, shots, lo, hi, P, g, 2) for g, (lo, hi) in enumerate(D.shard_ranges(n, P, q))]
+    slabs = D.LocalShardedLRE(cs).step([counts[c.w_lo:c.w_hi] for c in cs], None)
+    full = C.step_two(C.step_one(counts, n, shots), n)
+    d, S = 1 << n, (1 << n) // P
+    for g, slab in enumerate(slabs):
+        for r in range(0, d, 5):
             cols = ((r // S) ^ g) * S + np.arange(S)
             np.testing.assert_allclose(slab[r], full[r, cols], rtol=1e-12, atol=1e-15)
