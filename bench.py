@@ -717,6 +717,7 @@ def run_dist(args, rank: int, world: int, local: int):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
     dist.init_process_group("nccl", device_id=dev)
     n, shots, seed = args.n, args.shots, args.seed
     q = int(_lib.load().lre_shard_quantum(n))
