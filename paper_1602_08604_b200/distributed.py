@@ -87,18 +87,21 @@ class DeviceCompute:
         ws = ctypes.c_size_t(0)
         _lib.check(_lib.load().lre_step1_workspace(n, shots, w_lo, w_hi, ctypes.byref(ws)), "lre_step1_workspace")
         self.ws_bytes = int(ws.value)
-        self.ws = torch.empty(max(self.ws_bytes, 256), dtype=torch.uint8, device=self.device)
         d = 1 << n
         self.m_lo, self.m_hi = mask_range(n, world, rank)
         S = self.m_hi - self.m_lo
+        # mu, the received numerators and theta live in the step-(i) workspace, dead once
+        # the partial numerators are written (n = 14 at P = 1: 147 GB of counts + 22 GB)
+        mu_b, recv_b, th_b = 16 * d * S, 8 * S * d, 8 * S * d
+        self.ws = torch.empty(max(self.ws_bytes, mu_b + recv_b + th_b, 256), dtype=torch.uint8, device=self.device)
         self.K = default_chunks(n, world) if chunks is None else int(chunks)
         log_p, log_k = world.bit_length() - 1, self.K.bit_length() - 1
         self.layout = _lib.MASK_CHUNKED(log_p, log_k) if self.K > 1 else _lib.MASK_MAJOR
         self.chunk_elems = (S // self.K) * d
         self.num = torch.empty(4**n, dtype=torch.int64, device=self.device)
-        self.recv = torch.empty(S * d, dtype=torch.int64, device=self.device)
-        self.theta = torch.empty(S * d, dtype=torch.float64, device=self.device)
-        self.mu = torch.empty((d, S), dtype=torch.complex128, device=self.device)
+        self.mu = self.ws[:mu_b].view(torch.complex128).view(d, S)
+        self.recv = self.ws[mu_b:mu_b + recv_b].view(torch.int64)
+        self.theta = self.ws[mu_b + recv_b:mu_b + recv_b + th_b].view(torch.float64)
 
     def stream(self):
         return self.torch.cuda.current_stream(self.device)

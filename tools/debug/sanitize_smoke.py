@@ -1,8 +1,10 @@
 """Small instances of every product kernel, for compute-sanitizer
 (memcheck / racecheck / synccheck):
     compute-sanitizer --tool memcheck python tools/debug/sanitize_smoke.py
-Set LRE_ASM_BUDGET_KB=8 to route n = 10 assembly through the 2-CTA cluster
-kernel (used at n = 14 by default)."""
+Round 2 adds: the 8-CTA-cluster assembly (n = 11: SPLIT and FULL mask blocks,
+whole range and chunked slabs), the mask-major final pass, the fp64 frequency
+folds (device probabilities and a host-streamed source), one-pass streaming.
+Set LRE_ASM=legacy to route mask-major assembly through the round-1 kernels."""
 import sys
 
 import numpy as np
@@ -37,6 +39,29 @@ def main():
     res = lre.reconstruct(rec, project=True, as_tensor=True)
     M.evaluate_errors(lre.StateDescriptor("ghz", 6), res.rho, res.mu, n0=3.0)
     M.hs_squared_distance(res.mu, torch.from_numpy(rho).cuda())
+    # round 2: n = 11 (cluster assembly incl. FULL-mode blocks, mask-major final pass)
+    rec = lre.sample_counts(lre.StateDescriptor("ghz", 11), 40, seed=6)
+    lre.reconstruct(rec, project=False)
+    from paper_1602_08604_b200 import distributed as D
+
+    comp = D.DeviceCompute(11, 40, 0, 3**11, 1, 0, torch.device("cuda", 0), chunks=4)
+    D.LocalShardedLRE([comp]).step([rec.counts], rec.lre_dtype)
+    # fp64 frequency sources: device probabilities and a host-streamed duck source
+    lre.reconstruct(lre.ExactFrequencies(lre.StateDescriptor("random", 5, state_seed=7)), project=False)
+
+    class Src:
+        n, num_settings = 8, 3**8
+
+        def frequencies(self, a, b):
+            return np.full((b - a, 256), 1.0 / 256)
+
+    plan = lre.F64Plan(8, chunk_bytes=3**6 * 256 * 8)
+    plan.step1(Src(), torch.cuda.current_stream())
+    # one-pass streaming plan (n = 6)
+    r6 = lre.sample_counts(lre.StateDescriptor("w", 6), 100, seed=8)
+    p6 = lre.LREPlan(6, 100, with_mu=False)
+    p6.stage(r6.counts, r6.lre_dtype, 0, 3**6, torch.cuda.current_stream())
+    p6.finish(torch.cuda.current_stream())
     torch.cuda.synchronize()
     print("sanitize smoke ok")
 
