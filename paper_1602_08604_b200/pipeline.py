@@ -156,8 +156,7 @@ def to_device_record(record_or_source, device=None, stream=None) -> DeviceRecord
             counts = counts.astype(compact_dtype(int(rec.shots)))
         elif counts.dtype not in (np.uint8, np.uint16, np.int32, np.int64):
             counts = counts.astype(np.int64)  # int8/int16/uint32/...: exact in int64, validated below
-        host = torch.from_numpy(np.ascontiguousarray(counts))
-        dcounts = host.to(dev, non_blocking=False)
+        dcounts = _host_to_device(np.ascontiguousarray(counts), dev)
         drec = DeviceRecord(n=n, shots=int(rec.shots), counts=dcounts, seed=rec.seed, state=rec.state)
         drec.validate(stream)
         rec._validated = True
@@ -167,6 +166,31 @@ def to_device_record(record_or_source, device=None, stream=None) -> DeviceRecord
         "OutcomeRecord or a dyadic StateDescriptor (frequency sources go through reconstruct / "
         "step_one_least_squares)"
     )
+
+
+def _host_to_device(counts: np.ndarray, dev, chunk_bytes: int = 1 << 28):
+    """A host record into HBM through two pinned staging buffers (a host-side memcpy into
+    one while the other's H2D copy runs on a side stream) instead of one blocking
+    pageable copy; small records take the direct copy."""
+    torch = _torch()
+    host = torch.from_numpy(counts)
+    if counts.nbytes <= chunk_bytes:
+        return host.to(dev)
+    out = torch.empty(tuple(counts.shape), dtype=host.dtype, device=dev)
+    rows_per = max(1, chunk_bytes // max(1, counts.strides[0]))
+    pinned = [torch.empty((rows_per,) + tuple(counts.shape[1:]), dtype=host.dtype, pin_memory=True) for _ in range(2)]
+    copy = torch.cuda.Stream(dev)
+    done = [torch.cuda.Event() for _ in range(2)]
+    for k, lo in enumerate(range(0, counts.shape[0], rows_per)):
+        hi = min(counts.shape[0], lo + rows_per)
+        b = k % 2
+        done[b].synchronize()  # the previous copy out of this staging buffer has finished
+        pinned[b][: hi - lo].copy_(host[lo:hi])
+        with torch.cuda.stream(copy):
+            out[lo:hi].copy_(pinned[b][: hi - lo], non_blocking=True)
+            done[b].record(copy)
+    torch.cuda.current_stream(dev).wait_stream(copy)
+    return out
 
 
 def counts_from_outcomes(outcomes, n: int, shots: int, out=None, stream=None):
