@@ -1506,22 +1506,39 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
         const int64_t v0 = blk << 10;
         uint32_t mh, ah;  // mask / a bits of qubits 2 .. n-5 (natural_to_ma of the block index)
         natural_to_ma((uint64_t)blk, mh, ah);
+        // four consecutive v per thread: one 16-byte (int32) or two (int64) loads per
+        // plane, all six planes in flight before any arithmetic
+        const int vb = 4 * threadIdx.x;
+        Ta x[6][4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int vl = threadIdx.x + 256 * k;
-            Ta x[6];
+        for (int r = 0; r < 3; ++r)
 #pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                for (int b = 0; b < 2; ++b) {
-                    const int64_t row = r;
-                    x[2 * r + b] = (row >= a.alo && row < a.ahi)
-                                       ? (Ta)vload<Tin>(in + (row - a.xa0) * rstride + (int64_t)b * V + v0 + vl)
-                                       : (Ta)0;
+            for (int b = 0; b < 2; ++b) {
+                const bool ok = r >= a.alo && r < a.ahi;
+                const Tin *p = in + ((int64_t)r - a.xa0) * rstride + (int64_t)b * V + v0 + vb;
+                if constexpr (sizeof(Tin) == 4) {
+                    const int4 q = ok ? __ldcs(reinterpret_cast<const int4 *>(p)) : make_int4(0, 0, 0, 0);
+                    x[2 * r + b][0] = (Ta)q.x;
+                    x[2 * r + b][1] = (Ta)q.y;
+                    x[2 * r + b][2] = (Ta)q.z;
+                    x[2 * r + b][3] = (Ta)q.w;
+                } else {
+                    const longlong2 q0 = ok ? __ldcs(reinterpret_cast<const longlong2 *>(p)) : make_longlong2(0, 0);
+                    const longlong2 q1 = ok ? __ldcs(reinterpret_cast<const longlong2 *>(p) + 1) : make_longlong2(0, 0);
+                    x[2 * r + b][0] = (Ta)q0.x;
+                    x[2 * r + b][1] = (Ta)q0.y;
+                    x[2 * r + b][2] = (Ta)q1.x;
+                    x[2 * r + b][3] = (Ta)q1.y;
                 }
-            const Ta D[4] = {(x[0] + x[1]) + (x[2] + x[3]) + (x[4] + x[5]), x[0] - x[1], x[2] - x[3], x[4] - x[5]};
-            uint32_t m5, a5;
-            natural_to_ma((uint64_t)vl, m5, a5);
+            }
+        uint32_t mt4, at4;  // qubits above the lowest of v = vb + e
+        natural_to_ma((uint64_t)threadIdx.x, mt4, at4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const Ta D[4] = {(x[0][e] + x[1][e]) + (x[2][e] + x[3][e]) + (x[4][e] + x[5][e]), x[0][e] - x[1][e],
+                             x[2][e] - x[3][e], x[4][e] - x[5][e]};
+            // lowest qubit digit e = I, X, Y, Z -> (m, a) bits (0,0), (1,0), (1,1), (0,1)
+            const uint32_t m5 = (mt4 << 1) | (uint32_t)(e == 1 || e == 2), a5 = (at4 << 1) | (uint32_t)(e >= 2);
 #pragma unroll
             for (int d = 0; d < 4; ++d) {
                 double val;
