@@ -344,6 +344,24 @@ __device__ __forceinline__ void cluster_arrive_relaxed() {
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
+#ifdef LRE_X8_PROFILE
+// phase timestamps of the first 64 blocks of every CTA (debug builds only):
+// [cta][block][phase] with phases 0 top, 1 after wait, 2 pushed, 3 data in, 4 WHT done, 5 write done
+__device__ unsigned long long g_x8_prof[148 * 2][64][6];
+#define X8_T(ph)                                                                           \
+    do {                                                                                   \
+        if (t == 0 && it_ < 64) {                                                          \
+            unsigned long long now_;                                                       \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now_));                      \
+            g_x8_prof[blockIdx.x][it_][ph] = now_;                                         \
+        }                                                                                  \
+    } while (0)
+#else
+#define X8_T(ph) \
+    do {         \
+    } while (0)
+#endif
+
 struct X8Args {
     const double *theta;  // mask-major slice: theta[(m - m_begin) * 2^n + a]
     int64_t m_begin;
@@ -428,11 +446,14 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
     }
     uint32_t parity = 0;
     bool first = true;
-    for (; u < a.units; u += ncl, parity ^= 1) {
+    int it_ = 0;
+    for (; u < a.units; u += ncl, parity ^= 1, ++it_) {
         const uint32_t m0 = (uint32_t)(a.m_begin + u * 8);
         const int64_t smask = a.S - 1;
+        X8_T(0);
         if (!first) cluster_wait();  // every CTA has finished reading its buffer for the previous block
         first = false;
+        X8_T(1);
         if (split) {
             // ---- push: twist + 3-bit butterfly of this CTA's mask, eighth k -> CTA k ----
             if (t == 0) mbar_expect_tx(barR, (uint32_t)D * sizeof(double));
@@ -501,7 +522,9 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
                 for (int k = 0; k < 8; ++k)
                     st_async_v2(mapa_u32(F_s + off, k), g[q][0][k], g[q][1][k], mapa_u32(bar_s, k));
             }
+            X8_T(2);
             mbar_wait(barR, parity);
+            X8_T(3);
             // ---- WHT over a' bits 1 .. L-2 of the 8 eighths (this CTA's k = rank) ----
             {  // bits 1..4: 32 consecutive elements per thread (16-byte accesses, conflict-free)
                 const int arr = t / (E / 32), blk = t % (E / 32);
@@ -551,6 +574,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
                 }
             }
             __syncthreads();
+            X8_T(4);
             // ---- next block's theta into registers (in flight during the write phase) ----
             const int cb0 = b0, cb1 = b1, cb2 = b2;
             const int64_t un = u + ncl;
@@ -686,6 +710,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
                 }
             }
         }
+        X8_T(5);
         cluster_arrive_relaxed();  // this CTA is done reading its own buffer (and, FULL mode, the partners')
     }
     if (!first) cluster_wait();  // partners may still read this CTA's shared memory (FULL mode)
@@ -753,6 +778,14 @@ int assemble_impl(const double *theta, int layout, int n, int64_t m_begin, int64
 // masks [slab_begin, slab_begin + slab_masks): mu_slab[r * slab_masks + c] =
 // mu[r, ((r / slab_masks) ^ (slab_begin / slab_masks)) * slab_masks + c] —
 // one chunk of a rank's slice assembled as soon as its reduce-scatter chunk lands
+#ifdef LRE_X8_PROFILE
+extern "C" int lre_x8_profile_dump(void *host, size_t bytes) {
+    return cudaMemcpyFromSymbol(host, g_x8_prof, bytes < sizeof(g_x8_prof) ? bytes : sizeof(g_x8_prof)) == cudaSuccess
+               ? 0
+               : 2;
+}
+#endif
+
 int assemble_slab_impl(const double *theta, int n, int64_t m_begin, int64_t m_end, int64_t slab_begin,
                        int64_t slab_masks, double *mu, cudaStream_t s) {
     const int64_t masks = m_end - m_begin;
