@@ -179,6 +179,31 @@ class ShardedLRE:
         return mu
 
 
+    def gather_mu(self, dst: int = 0):
+        """The dense row-major mu on rank `dst` (None elsewhere): the slabs gathered over the
+        process group (SURVEY §8(e) optional follow-on: one GPU then runs step (iii)).  Rank g's
+        slab holds, in row block b, the column block b ^ g."""
+        import torch
+        import torch.distributed as dist
+
+        c = self.c
+        slab = c.mu if isinstance(c.mu, torch.Tensor) else torch.from_numpy(c.mu)
+        slab = torch.view_as_real(slab.contiguous())  # complex128 as float64 pairs (gloo has no complex)
+        rank = dist.get_rank(self.group)
+        P = c.world
+        d = 1 << c.n
+        S = d // P
+        gathered = [torch.empty_like(slab) for _ in range(P)] if rank == dst else None
+        dist.gather(slab, gathered, dst=dst, group=self.group)
+        if rank != dst:
+            return None
+        mu = torch.empty((d, d), dtype=torch.complex128, device=slab.device)
+        for g, sl in enumerate(torch.view_as_complex(x) for x in gathered):
+            for b in range(P):
+                mu[b * S:(b + 1) * S, (b ^ g) * S:((b ^ g) + 1) * S] = sl[b * S:(b + 1) * S]
+        return mu
+
+
 class LocalShardedLRE:
     """One process driving P devices (reconstruct(..., devices=P)): the same chunked
     exchange, with the reduce-scatter done as peer-to-peer slice copies (NVLink)

@@ -108,8 +108,12 @@ def _worker(rank, world, port, n, shots, counts, out_path, chunks=1):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     lo, hi = D.shard_ranges(n, world, 3 ** min(n, 7))[rank]
     comp = OracleCompute(n, shots, lo, hi, world, rank, chunks)
-    mu = D.ShardedLRE(comp).step(counts[lo:hi], None)
+    runner = D.ShardedLRE(comp)
+    mu = runner.step(counts[lo:hi], None)
     np.save(f"{out_path}.{rank}.npy", mu)
+    full = runner.gather_mu(dst=0)  # dense mu on rank 0 (step iii input)
+    if rank == 0:
+        np.save(f"{out_path}.full.npy", full.numpy())
     dist.destroy_process_group()
 
 
@@ -122,6 +126,7 @@ def test_gloo_exchange_matches_single_rank(tmp_path, rng, n, world, chunks):
     mp.spawn(_worker, args=(world, _free_port(), n, shots, counts, out, chunks), nprocs=world, join=True)
     theta = C.step_one(counts, n, shots)
     full = C.step_two(theta, n)
+    np.testing.assert_allclose(np.load(f"{out}.full.npy"), full, rtol=1e-12, atol=1e-15)
     d, S = 1 << n, (1 << n) // world
     for g in range(world):
         slab = np.load(f"{out}.{g}.npy")
