@@ -37,6 +37,8 @@
 
 namespace lre {
 
+#include "lre_y1rank.inc"
+
 // ===========================================================================
 // epilogue shared by both kernels
 // ===========================================================================
@@ -126,6 +128,12 @@ struct P1Args {
     Final f;             // f.kind == OUT_INTER: Y1 int32 tile-major
     int debug_no_l2;     // diagnostics only (LRE_P1_DEBUG=noL2 / noL1): skip L2 / L1 work, output invalid
     int debug_no_l1;
+    // split Y1 (Q = 7, SMALL): every value's low 16 bits in lo[tile][16384] (int16), and for the
+    // 1156 indices with >= 4 identity digits (the only ones that can exceed int16) the high part
+    // in hi[tile][2048] at their rank; f.out unused
+    int split16;
+    int16_t *lo;
+    int16_t *hi;
 };
 
 // --- packed loads: 8 consecutive counts -> 4 words (c[2k] | c[2k+1] << 16) ---
@@ -275,7 +283,8 @@ __device__ __forceinline__ void l1_wide(RowLd ld, Sink sink) {
 }
 
 // L2: the 27 x 8 staged values (rb = a1*9 + a2*3 + a3, g = b1*4 + b2*2 + b3)
-// of one staged column -> sink(D3, v[16]) with v index D1*4 + D2.
+// of one staged column -> sink(D3, v[16], is_I) with v index D1*4 + D2 and
+// is_I a compile-time std::bool_constant<D3 == 0>.
 template <typename T, int STRIDE, typename Sink>
 __device__ __forceinline__ void l2_transform(const T *st, Sink sink) {
     int32_t Iacc[16];
@@ -310,9 +319,9 @@ __device__ __forceinline__ void l2_transform(const T *st, Sink sink) {
                 v[D1 * 4 + D2] = z0[D2] - z1[D2];
             }
         }
-        sink(a3 + 1, v);
+        sink(a3 + 1, v, std::false_type{});
     }
-    sink(0, Iacc);
+    sink(0, Iacc, std::true_type{});
 }
 
 // numerators (int32 or int64) in natural order -> final theta / int64 numerators
@@ -364,6 +373,15 @@ __device__ __forceinline__ int staged_col_to_dlo(int col) {
 __device__ __forceinline__ void p1_step_barrier() { asm volatile("barrier.sync 0;" ::: "memory"); }
 
 // Sub-tile s of this CTA -> tile, top setting digit r1, top outcome bit b1
+// compile-time loop: f(std::integral_constant<int, i>) for i = 0 .. N-1
+template <int I, int N, typename F> __device__ __forceinline__ void static_for_impl(F &&f) {
+    if constexpr (I < N) {
+        f(std::integral_constant<int, I>{});
+        static_for_impl<I + 1, N>(f);
+    }
+}
+template <int N, typename F> __device__ __forceinline__ void static_for(F &&f) { static_for_impl<0, N>(f); }
+
 struct SubTile {
     int64_t aH, c;
     int r1, b1;
@@ -391,12 +409,36 @@ __device__ __forceinline__ void l2_subtile_rb(const P1Args &a, const SubTile &st
                                               int32_t *oi) {
     constexpr int STRIDE = Stage<SMALL>::STRIDE;
     const int dlo = staged_col_to_dlo(col);
-    int32_t *out = reinterpret_cast<int32_t *>(a.f.out) +
-                   (((st.aH - a.out_aH0) * a.C + st.c) << (2 * Q)) + dlo;
+    const int64_t tile = (st.aH - a.out_aH0) * a.C + st.c;
+    int32_t *out = reinterpret_cast<int32_t *>(a.f.out) + (tile << (2 * Q)) + dlo;
     int32_t *tc = tmp + col, *oc = oi + col;
-    l2_transform<typename Stage<SMALL>::T, STRIDE>(stage + col, [&](int D3, const int32_t(&v)[16]) {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
+    // split Y1 (make_plan): the value at u * 64 + dlo (u = top, D1, D2, D3) has a high part
+    // iff zc(dlo) >= 4 - zc(u); ZC_U is known at compile time, so most stores need no test.
+    int16_t *lo = a.lo + (tile << 14) + dlo;
+    int16_t *hi = a.hi + (tile << 11);
+    const uint32_t lrpack = (Q == 7 && a.split16) ? g_y1_lrpack[dlo] : 0u;
+    auto put = [&](int idx_hi, auto zc_u, int32_t val) {  // idx_hi = u * 64
+        constexpr int T = 4 - decltype(zc_u)::value;
+        if (Q != 7 || !a.split16) {
+            out[idx_hi] = val;
+        } else {
+            const int16_t l16 = (int16_t)val;
+            lo[idx_hi] = l16;
+            if constexpr (T < 4) {
+                const int h16 = (val - (int32_t)l16) >> 16;
+                const int uoff = c_y1_uoff[idx_hi >> 6];
+                if constexpr (T <= 0) {
+                    hi[uoff + dlo] = (int16_t)h16;
+                } else {
+                    const int lr = (lrpack >> (8 * (T - 1))) & 0xFF;
+                    if (lr != 0xFF) hi[uoff + lr] = (int16_t)h16;
+                }
+            }
+        }
+    };
+    l2_transform<typename Stage<SMALL>::T, STRIDE>(stage + col, [&](int D3, const int32_t(&v)[16], auto is_i) {
+        static_for<16>([&](auto K) {
+            constexpr int k = decltype(K)::value;
             const int r = k * 4 + D3;  // core digits D1 D2 D3
             if constexpr (Q == 6) {
                 out[r * 64] = v[k];
@@ -406,11 +448,13 @@ __device__ __forceinline__ void l2_subtile_rb(const P1Args &a, const SubTile &st
                 const int32_t u = tc[r * 64];
                 int32_t acc = u + v[k];
                 if constexpr (R1 > 0) acc += oc[r * 64];
+                // identity digits among D1 D2 D3 (k = D1 * 4 + D2 is unrolled)
+                using ZcR = std::integral_constant<int, ((k >> 2) == 0) + ((k & 3) == 0) + (decltype(is_i)::value ? 1 : 0)>;
                 if constexpr (R1 < 2) oc[r * 64] = acc;
-                else out[r * 64] = acc;                    // top digit I
-                out[(R1 + 1) * 4096 + r * 64] = u - v[k];  // top digit X / Y / Z
+                else put(r * 64, std::integral_constant<int, ZcR::value + 1>{}, acc);  // top digit I
+                put((R1 + 1) * 4096 + r * 64, ZcR{}, u - v[k]);                       // top digit X / Y / Z
             }
-        }
+        });
     });
 }
 
@@ -1101,8 +1145,10 @@ constexpr int VF3_WARPS = VF3_W;
 constexpr int VF3_GROUP_CHUNKS = 72 * 8;  // 16-byte chunks per r1 group (72 lines x 128 B)
 constexpr int VF3_SLOTS = VF3_S;
 
-template <bool FINAL>
+// Tin = int16_t: the low halves of a split Y1 (lines of 32 v are 64 bytes); int32 otherwise
+template <bool FINAL, typename Tin = int32_t>
 __global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const VArgs a) {
+    constexpr int CPL = 32 * (int)sizeof(Tin) / 16;  // 16-byte chunks per line of 32 v
     extern __shared__ __align__(16) int4 vsm4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int4 *ring = vsm4 + warp * VF3_SLOTS * VF3_GROUP_CHUNKS;
@@ -1114,7 +1160,7 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const 
     const int64_t V = a.V;
     const int64_t nvb = V >> 5;
     const int64_t ntask = a.nA * a.nB * nvb;
-    const int32_t *in = reinterpret_cast<const int32_t *>(a.in);
+    const Tin *in = reinterpret_cast<const Tin *>(a.in);
     const int64_t gw = (int64_t)blockIdx.x * VF3_WARPS + warp, nw = (int64_t)gridDim.x * VF3_WARPS;
     const int my_tasks = gw < ntask ? (int)((ntask - 1 - gw) / nw) + 1 : 0;
     const int nq = my_tasks * 3;
@@ -1132,15 +1178,16 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const 
             task_coords(q / 3, A, B, v0);
             const int r1 = q % 3;
             const int64_t row0 = A * 27 + r1 * 9;
-            const int32_t *p0 = in + ((row0 - a.xa0) * a.ncol + B * 8) * V + v0;
+            const Tin *p0 = in + ((row0 - a.xa0) * a.ncol + B * 8) * V + v0;
             int4 *slot = ring + (q % VF3_SLOTS) * VF3_GROUP_CHUNKS;
 #pragma unroll
-            for (int k = 0; k < 18; ++k) {
+            for (int k = 0; k < 72 * CPL / 32; ++k) {
                 const int id = lane + 32 * k;
-                const int L = id >> 3, c = id & 7, j = L >> 3, s = L & 7;
+                const int L = id / CPL, c = id % CPL, j = L >> 3, s = L & 7;
                 const int64_t row = row0 + j;
                 const bool ok = row >= a.alo && row < a.ahi;
-                cp_async16(slot + id, ok ? (const void *)(p0 + (j * a.ncol + s) * V + c * 4) : (const void *)in,
+                cp_async16(slot + id,
+                           ok ? (const void *)(p0 + (j * a.ncol + s) * V + c * (16 / (int)sizeof(Tin))) : (const void *)in,
                            ok ? 16 : 0);
             }
         }
@@ -1156,8 +1203,8 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const 
         const int r1 = q % 3;
         int64_t A, B, v0;
         task_coords(q / 3, A, B, v0);
-        const int32_t *st = reinterpret_cast<const int32_t *>(ring + (q % VF3_SLOTS) * VF3_GROUP_CHUNKS);
-        auto x = [&](int j, int s) -> int32_t { return st[(j * 8 + s) * 32 + lane]; };
+        const Tin *st = reinterpret_cast<const Tin *>(ring + (q % VF3_SLOTS) * VF3_GROUP_CHUNKS);
+        auto x = [&](int j, int s) -> int32_t { return (int32_t)st[(j * 8 + s) * 32 + lane]; };
         const int64_t v = v0 + lane;
         int32_t *out = nullptr;
         if constexpr (!FINAL) out = reinterpret_cast<int32_t *>(a.f.out) + ((A - a.ya0) * a.nB + B) * 64 * V + v;
@@ -1227,6 +1274,7 @@ struct Pass {
     int64_t alo, ahi; // valid input rows (previous-level units)
     int64_t A0, nA;   // output row groups computed
     size_t out_bytes; // intermediate output bytes (0 for the final pass)
+    size_t hi_off;    // split Y1: byte offset of the high-part plane in the output buffer
 };
 
 // byte offset of the int64 numerators a one-pass streaming stage leaves in the workspace
@@ -1240,7 +1288,28 @@ struct Plan {
     std::vector<Pass> p;
     size_t ws_bytes = 0;
     size_t off[2] = {0, 0};  // ping-pong buffers for intermediates
+    int split = 0;           // split Y1 storage (below)
 };
+
+// Split Y1 storage.  Pass 1 (Q = 7) values satisfy |Y1[v]| <= shots * 3^zc(v),
+// zc(v) = identity digits of the 7-qubit index v.  With shots * 27 <= 32767
+// every value with zc <= 3 fits int16, so Y1 is stored as an int16 plane of
+// low halves (lo, 2 B per value) plus, for the 1156 of 16384 indices per tile
+// with zc >= 4, the high part hi = (y - lo) / 65536 in a compact int16 plane
+// [tile][2048] (lre_y1rank.inc).  Both planes go through the same Q = 3 folds
+// (linear, so lo and hi chains stay exact: lo after L levels is bounded by
+// 3^L * 32768), and y1_merge_kernel recombines lo + 65536 * hi at the level
+// the final pass reads.  Pass 1 writes and pass 2 reads 10.3 GB instead of
+// 18.3 GB at n = 14.  Requires: rows of the record sum to shots (the same
+// contract the int32 bounds rest on; lre_validate_counts checks it).
+static bool split_allowed() {
+    static const bool on = [] {
+        const char *e = getenv("LRE_Y1SPLIT");
+        const char *v = getenv("LRE_P1");
+        return !(e && e[0] == '0') && !(v && !strcmp(v, "ring"));
+    }();
+    return on;
+}
 
 // first-pass width: the tile pass when it applies, else vfold from raw counts
 // vfold passes consume at most two qubits: a thread then needs 36 loads
@@ -1293,6 +1362,21 @@ Plan make_plan(int n, int64_t shots, int dtype, int64_t w_begin, int64_t w_end) 
         lo = ps.A0;
         hi = ps.A0 + ps.nA;
         done += ps.q;
+    }
+    {
+        const size_t np = pl.p.size();
+        bool sp = split_allowed() && np >= 3 && pl.p[0].kind == 0 && pl.p[0].q == 7 && shots >= 1 &&
+                  shots * 27 <= 32767 && pl.p[np - 1].in_dtype == LRE_I32;
+        for (size_t i = 1; sp && i + 1 < np; ++i) sp = pl.p[i].q == 3 && !pl.p[i].acc64;
+        if (sp) {
+            pl.split = 1;
+            for (size_t i = 0; i + 1 < np; ++i) {
+                const size_t eb = i == 0 ? 2 : 4;  // int16 Y1, int32 later levels
+                const size_t elems = pl.p[i].out_bytes / 4;
+                pl.p[i].hi_off = (elems * eb + 255) & ~(size_t)255;
+                pl.p[i].out_bytes = pl.p[i].hi_off + elems / 8 * eb;
+            }
+        }
     }
     // intermediates alternate between two buffers
     size_t need[2] = {0, 0};
@@ -1449,6 +1533,7 @@ static cudaError_t launch_vfold(const VArgs &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+template <typename Tin = int32_t>
 static cudaError_t launch_vfold3(const VArgs &a, cudaStream_t s) {
     const size_t smem = (size_t)VF3_WARPS * VF3_SLOTS * VF3_GROUP_CHUNKS * sizeof(int4);
     const int64_t tasks = a.nA * a.nB * (a.V >> 5);
@@ -1456,10 +1541,11 @@ static cudaError_t launch_vfold3(const VArgs &a, cudaStream_t s) {
                                                                 (int64_t)num_sms() * VF3_MINB));
     cudaError_t e;
     if (a.f.kind == OUT_INTER) {
-        e = cudaFuncSetAttribute(vfold3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(vfold3_kernel<false, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        vfold3_kernel<false><<<(unsigned)grid, 32 * VF3_WARPS, smem, s>>>(a);
+        vfold3_kernel<false, Tin><<<(unsigned)grid, 32 * VF3_WARPS, smem, s>>>(a);
     } else {
+        if constexpr (!std::is_same<Tin, int32_t>::value) return cudaErrorInvalidValue;
         e = cudaFuncSetAttribute(vfold3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         vfold3_kernel<true><<<(unsigned)grid, 32 * VF3_WARPS, smem, s>>>(a);
@@ -1610,6 +1696,23 @@ static cudaError_t run_vfold(int q, int in_dtype, int acc64, const VArgs &a, cud
     }
 }
 
+// Split Y1 (make_plan): lo[row][v] += 65536 * hi[row][(v >> 14) * 2048 + rank(v & 16383)]
+// over the exception indices, in place on the int32 level the final pass reads.
+// One thread per exception: hi is read densely, lo touched at 1156 of 16384 v.
+__global__ void __launch_bounds__(256) y1_merge_kernel(int32_t *__restrict__ lo, const int32_t *__restrict__ hi,
+                                                       int64_t rows, int64_t V) {
+    const int64_t per_row = (V >> 14) * LRE_Y1_EXC;
+    const int64_t total = rows * per_row;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = i / per_row, rem = i - row * per_row;
+        const int64_t h = rem / LRE_Y1_EXC;
+        const int rk = (int)(rem - h * LRE_Y1_EXC);
+        int32_t *p = lo + row * V + (h << 14) + g_y1_exc_v[rk];
+        const int64_t y = (int64_t)*p + 65536 * (int64_t)hi[row * (V >> 3) + (h << 11) + rk];
+        *p = (int32_t)y;
+    }
+}
+
 // Run passes [first, last) of `pl` (computed rows) with intermediates laid out
 // as in `lay` (== pl for one-shot shards; the full-range plan for streaming).
 static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last, const void *counts,
@@ -1635,6 +1738,13 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
         cudaError_t e;
         if (ps.kind == 0) {
             P1Args a;
+            a.split16 = 0;
+            a.lo = a.hi = nullptr;
+            if (lay.split) {
+                a.split16 = 1;
+                a.lo = reinterpret_cast<int16_t *>(f.out);
+                a.hi = reinterpret_cast<int16_t *>((char *)f.out + ls.hi_off);
+            }
             a.counts = counts;
             a.rowlen = (int64_t)1 << n;
             a.row_base = row_base;
@@ -1681,7 +1791,31 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             a.f = f;
             const bool fmm = fin && ps.q == 1 && layout_is_mask_major(layout) && a.V >= 1024 && a.A0 == 0 && a.nA == 1 &&
                              a.nB == 1 && (ps.in_dtype == LRE_I32 || ps.in_dtype == LRE_I64);
-            e = fmm ? launch_final_mm(ps.in_dtype, ps.acc64, a, stream) : run_vfold(ps.q, ps.in_dtype, ps.acc64, a, stream);
+            if (lay.split && !fin) {
+                // lo plane (int16 Y1 at pass 2), then the hi plane: V / 8 lanes per row
+                e = i == 1 ? launch_vfold3<int16_t>(a, stream) : launch_vfold3<int32_t>(a, stream);
+                if (e == cudaSuccess) {
+                    VArgs h = a;
+                    h.in = (const char *)in + lay.p[i - 1].hi_off;
+                    h.f.out = (char *)f.out + ls.hi_off;
+                    h.V = a.V / 8;
+                    h.logV = a.logV - 3;
+                    e = i == 1 ? launch_vfold3<int16_t>(h, stream) : launch_vfold3<int32_t>(h, stream);
+                }
+                if (e == cudaSuccess && i + 2 == pl.p.size()) {
+                    const int64_t rows = ps.nA * a.nB, Vout = a.V * 64;
+                    const int64_t total = rows * (Vout >> 14) * LRE_Y1_EXC;
+                    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+                    y1_merge_kernel<<<(unsigned)blocks, 256, 0, stream>>>(
+                        reinterpret_cast<int32_t *>(f.out),
+                        reinterpret_cast<const int32_t *>((const char *)f.out + ls.hi_off), rows, Vout);
+                    count_launch();
+                    e = cudaGetLastError();
+                }
+            } else {
+                e = fmm ? launch_final_mm(ps.in_dtype, ps.acc64, a, stream)
+                        : run_vfold(ps.q, ps.in_dtype, ps.acc64, a, stream);
+            }
         }
         if (e != cudaSuccess) return e == cudaErrorInvalidValue ? LRE_EUNSUPPORTED : LRE_ECUDA;
         done += ps.q;
