@@ -134,6 +134,7 @@ struct P1Args {
     int split16;
     int16_t *lo;
     int16_t *hi;
+    int pipe;  // tile_pass_kernel stage hand-off: 1 = full/empty mbarriers, 0 = lockstep CTA barrier
 };
 
 // --- packed loads: 8 consecutive counts -> 4 words (c[2k] | c[2k+1] << 16) ---
@@ -505,6 +506,22 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
     const int rowlen = LOGN > 0 ? (1 << LOGN) : (int)a.rowlen;
     const bool l1 = warp < P1_L1_WARPS && tid < P1_ITEMS;
     const int rb = tid >> 3, g = tid & 7;
+    // Stage hand-off.  a.pipe (default): per-buffer full/empty mbarriers, so the
+    // L1 warps fill buffer s & 1 as soon as the L2 warps have drained sub-tile
+    // s - 2 and a slow step on either side is absorbed by the other instead of
+    // both waiting at a lockstep CTA barrier (ncu at n = 14: ~28 % of both
+    // sides' samples sat in that barrier).  LRE_P1_SYNC=bar: the lockstep form.
+    __shared__ __align__(8) uint64_t bars[4];  // full[2], empty[2]
+    if (a.pipe) {
+        if (tid == 0) {
+            mbar_init(&bars[0], 32 * P1_L1_WARPS);
+            mbar_init(&bars[1], 32 * P1_L1_WARPS);
+            mbar_init(&bars[2], 32 * P1_L2_WARPS);
+            mbar_init(&bars[3], 32 * P1_L2_WARPS);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
 
     auto item_base = [&](int s) -> const Tin * {
         const SubTile st = subtile_of<Q>(a, s);
@@ -536,6 +553,10 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
             }
         }
         for (int s = 0; s <= S; ++s) {
+            if (a.pipe) {
+                if (s == S) break;
+                if (s >= 2) mbar_wait(&bars[2 + (s & 1)], ((s >> 1) - 1) & 1);
+            }
             if (s < S && l1 && !a.debug_no_l1) {
                 T *rec = reinterpret_cast<T *>(smem + (s & 1) * ST::BYTES) + tid * STRIDE;
                 if constexpr (SMALL) {
@@ -580,7 +601,16 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
                             [&](int D6, const int32_t(&v)[16]) { stage_record<SMALL>(rec, D6, v); });
                 }
             }
-            p1_step_barrier();
+            if (a.pipe) mbar_arrive(&bars[s & 1]);
+            else p1_step_barrier();
+        }
+    } else if (a.pipe) {
+        for (int s = 0; s < S; ++s) {
+            mbar_wait(&bars[s & 1], (s >> 1) & 1);
+            if (!a.debug_no_l2)
+                l2_subtile<Q, SMALL>(a, subtile_of<Q>(a, s), reinterpret_cast<const T *>(smem + (s & 1) * ST::BYTES),
+                                     tid - 32 * P1_L1_WARPS, tmp, oi);
+            mbar_arrive(&bars[2 + (s & 1)]);
         }
     } else {
         for (int s = 0; s <= S; ++s) {
@@ -950,6 +980,7 @@ struct VArgs {
     int logV, lognB;  // V and nB are powers of two: index math by shifts (64-bit div/mod is ~100 instructions)
     int vf1_batch;  // Q = 1: issue all row loads of 4 elements first (LRE_VF1=0 disables; A/B only)
     Final f;
+    const int32_t *hi = nullptr;  // split Y1 high parts of the input (rows of V / 8) for the fused merge, or null
 };
 
 // final-store value: integers widen to int64 numerators, fp64 stays fp64
@@ -1197,20 +1228,34 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const 
 #pragma unroll
     for (int k = 0; k < VF3_SLOTS; ++k) issue(k);
     int32_t Iacc[16];
+    // int16 input: a task's lines are 64-byte halves of 128-byte lines whose other halves
+    // belong to the neighbouring warp's task.  Keep the CTA's warps in step (one named
+    // barrier per task while every warp still has one) so both halves are requested
+    // together: warps that drift apart re-fetch whole lines from DRAM (measured at n = 14:
+    // up to 2x the reads; with the barrier pass 2 reads 9.17 GB in 2.1 ms instead of 2.6 ms)
+    const int64_t gw_last = (int64_t)blockIdx.x * VF3_WARPS + VF3_WARPS - 1;
+    const int cta_tasks = gw_last < ntask ? (int)((ntask - 1 - gw_last) / nw) + 1 : 0;
     for (int q = 0; q < nq; ++q) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(VF3_SLOTS - 1) : "memory");
-        __syncwarp();
+        if constexpr (sizeof(Tin) == 2) {
+            if (q % 3 == 0 && q / 3 < cta_tasks) asm volatile("bar.sync 1, %0;" ::"n"(32 * VF3_WARPS) : "memory");
+        }
         const int r1 = q % 3;
         int64_t A, B, v0;
         task_coords(q / 3, A, B, v0);
+        const int64_t v = v0 + lane;
+        const int64_t orow = (A - a.ya0) * a.nB + B;
+        int32_t *out = nullptr;
+        if constexpr (!FINAL) out = reinterpret_cast<int32_t *>(a.f.out) + orow * 64 * V + v;
+        asm volatile("cp.async.wait_group %0;" ::"n"(VF3_SLOTS - 1) : "memory");
+        __syncwarp();
         const Tin *st = reinterpret_cast<const Tin *>(ring + (q % VF3_SLOTS) * VF3_GROUP_CHUNKS);
         auto x = [&](int j, int s) -> int32_t { return (int32_t)st[(j * 8 + s) * 32 + lane]; };
-        const int64_t v = v0 + lane;
-        int32_t *out = nullptr;
-        if constexpr (!FINAL) out = reinterpret_cast<int32_t *>(a.f.out) + ((A - a.ya0) * a.nB + B) * 64 * V + v;
         auto sink = [&](int d, int32_t y) {
-            if constexpr (!FINAL) out[(int64_t)d * V] = y;
-            else store_final(a.f, sfac, (uint64_t)(d * V + v), (int64_t)y);
+            if constexpr (!FINAL) {
+                out[(int64_t)d * V] = y;
+            } else {
+                store_final(a.f, sfac, (uint64_t)(d * V + v), (int64_t)y);
+            }
         };
         if (r1 == 0) {
 #pragma unroll
@@ -1541,9 +1586,10 @@ static cudaError_t launch_vfold3(const VArgs &a, cudaStream_t s) {
                                                                 (int64_t)num_sms() * VF3_MINB));
     cudaError_t e;
     if (a.f.kind == OUT_INTER) {
-        e = cudaFuncSetAttribute(vfold3_kernel<false, Tin>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        auto kern = vfold3_kernel<false, Tin>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        vfold3_kernel<false, Tin><<<(unsigned)grid, 32 * VF3_WARPS, smem, s>>>(a);
+        kern<<<(unsigned)grid, 32 * VF3_WARPS, smem, s>>>(a);
     } else {
         if constexpr (!std::is_same<Tin, int32_t>::value) return cudaErrorInvalidValue;
         e = cudaFuncSetAttribute(vfold3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1595,6 +1641,9 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
         // four consecutive v per thread: one 16-byte (int32) or two (int64) loads per
         // plane, all six planes in flight before any arithmetic
         const int vb = 4 * threadIdx.x;
+        // split Y1 (make_plan): positions of the four v's high parts, or 0xFFFF
+        uint2 hpos = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
+        if (a.hi) hpos = *reinterpret_cast<const uint2 *>(g_y1_pos + ((v0 + vb) & 16383));
         Ta x[6][4];
 #pragma unroll
         for (int r = 0; r < 3; ++r)
@@ -1617,6 +1666,20 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
                     x[2 * r + b][3] = (Ta)q1.y;
                 }
             }
+        if (a.hi && (hpos.x & hpos.y) != 0xFFFFFFFFu) {
+            const uint32_t hp[4] = {hpos.x & 0xFFFF, hpos.x >> 16, hpos.y & 0xFFFF, hpos.y >> 16};
+            const int64_t hrow = (((v0 + vb) >> 14) << 11);
+#pragma unroll
+            for (int r = 0; r < 3; ++r)
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    if (r < a.alo || r >= a.ahi) continue;
+                    const int32_t *h = a.hi + (((int64_t)r - a.xa0) * a.ncol + b) * (V >> 3) + hrow;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        if (hp[e] != 0xFFFF) x[2 * r + b][e] += (Ta)65536 * (Ta)__ldg(h + hp[e]);
+                }
+        }
         uint32_t mt4, at4;  // qubits above the lowest of v = vb + e
         natural_to_ma((uint64_t)threadIdx.x, mt4, at4);
 #pragma unroll
@@ -1696,6 +1759,15 @@ static cudaError_t run_vfold(int q, int in_dtype, int acc64, const VArgs &a, cud
     }
 }
 
+// The final pass runs final_mm_kernel (one-qubit fold straight into the mask-major layout)
+static bool final_is_mm(const Pass &ps, int layout, int n, int done) {
+    return ps.q == 1 && layout_is_mask_major(layout) && ipow(4, done) >= 1024 && ps.A0 == 0 && ps.nA == 1 &&
+           n - done == 1 && (ps.in_dtype == LRE_I32 || ps.in_dtype == LRE_I64);
+}
+static bool final_fuses_merge(const Plan &pl, size_t i, int layout, int n, int done) {
+    return pl.split && i + 1 == pl.p.size() && final_is_mm(pl.p[i], layout, n, done);
+}
+
 // Split Y1 (make_plan): lo[row][v] += 65536 * hi[row][(v >> 14) * 2048 + rank(v & 16383)]
 // over the exception indices, in place on the int32 level the final pass reads.
 // One thread per exception: hi is read densely, lo touched at 1156 of 16384 v.
@@ -1738,6 +1810,11 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
         cudaError_t e;
         if (ps.kind == 0) {
             P1Args a;
+            static const int pipe = [] {
+                const char *v = getenv("LRE_P1_SYNC");
+                return v && !strcmp(v, "bar") ? 0 : 1;
+            }();
+            a.pipe = pipe;
             a.split16 = 0;
             a.lo = a.hi = nullptr;
             if (lay.split) {
@@ -1789,8 +1866,10 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             }();
             a.vf1_batch = vf1;
             a.f = f;
-            const bool fmm = fin && ps.q == 1 && layout_is_mask_major(layout) && a.V >= 1024 && a.A0 == 0 && a.nA == 1 &&
-                             a.nB == 1 && (ps.in_dtype == LRE_I32 || ps.in_dtype == LRE_I64);
+            const bool fmm = fin && final_is_mm(ps, layout, n, done);
+            a.hi = nullptr;
+            if (fmm && lay.split)  // merge of the split high parts fused into the final pass
+                a.hi = reinterpret_cast<const int32_t *>((const char *)in + lay.p[i - 1].hi_off);
             if (lay.split && !fin) {
                 // lo plane (int16 Y1 at pass 2), then the hi plane: V / 8 lanes per row
                 e = i == 1 ? launch_vfold3<int16_t>(a, stream) : launch_vfold3<int32_t>(a, stream);
@@ -1802,7 +1881,7 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
                     h.logV = a.logV - 3;
                     e = i == 1 ? launch_vfold3<int16_t>(h, stream) : launch_vfold3<int32_t>(h, stream);
                 }
-                if (e == cudaSuccess && i + 2 == pl.p.size()) {
+                if (e == cudaSuccess && i + 2 == pl.p.size() && !final_fuses_merge(pl, i + 1, layout, n, done + ps.q)) {
                     const int64_t rows = ps.nA * a.nB, Vout = a.V * 64;
                     const int64_t total = rows * (Vout >> 14) * LRE_Y1_EXC;
                     const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
