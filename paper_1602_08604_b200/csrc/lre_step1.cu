@@ -1623,9 +1623,12 @@ static cudaError_t vfold_q(int q, const VArgs &a, cudaStream_t s) {
 // 4 x 1024 results in shared memory as [digit][m5][a5] every warp writes runs
 // of 32 consecutive doubles (256 B) of one mask row.  Reads: the six
 // (setting digit, outcome bit) planes of the input, 4 KB lines.
+struct longlong4_pair {
+    longlong2 a, b;
+};
 template <typename Tin, typename Ta, bool NUM>
 __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
-    __shared__ double st[4 * 32 * 33];
+    __shared__ int64_t st[4 * 32 * 33];  // exact numerators; theta = N * factor at write-out
     __shared__ double sfac[33];
     if constexpr (!NUM) stage_factors(sfac, a.f.fac);
     const Tin *in = reinterpret_cast<const Tin *>(a.in);
@@ -1633,52 +1636,72 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
     const int64_t V = a.V;  // 4^(n-1)
     const int64_t nblk = V >> 10;
     const int64_t rstride = a.ncol * V;
-    __syncthreads();
-    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const int vb = 4 * threadIdx.x;
+    // Block loads, software-pipelined: block blk + gridDim.x's planes are requested before
+    // this block's write-out.  Four consecutive v per thread: one 16-byte (int32) or two
+    // (int64) loads per plane.
+    using L = typename std::conditional<sizeof(Tin) == 4, int4, longlong4_pair>::type;
+    L ld[6];
+    // Split Y1 (make_plan): a block's 1024 v hold 16 whole 7-digit u blocks, whose high
+    // parts sit at the consecutive compact positions [P0, P1) of every plane row
+    // (lre_y1rank.inc, at most 376): thread t loads the six planes' high parts of
+    // exceptions P0 + t and P0 + t + 256 (coalesced across threads) with the planes.
+    int hx[2][6];
+    int hw[2];  // block-local v of this thread's exceptions, or -1
+    auto load = [&](int64_t blk) {
         const int64_t v0 = blk << 10;
-        uint32_t mh, ah;  // mask / a bits of qubits 2 .. n-5 (natural_to_ma of the block index)
-        natural_to_ma((uint64_t)blk, mh, ah);
-        // four consecutive v per thread: one 16-byte (int32) or two (int64) loads per
-        // plane, all six planes in flight before any arithmetic
-        const int vb = 4 * threadIdx.x;
-        // split Y1 (make_plan): positions of the four v's high parts, or 0xFFFF
-        uint2 hpos = make_uint2(0xFFFFFFFFu, 0xFFFFFFFFu);
-        if (a.hi) hpos = *reinterpret_cast<const uint2 *>(g_y1_pos + ((v0 + vb) & 16383));
-        Ta x[6][4];
 #pragma unroll
-        for (int r = 0; r < 3; ++r)
+        for (int i = 0; i < 6; ++i) {
+            const int r = i >> 1, b = i & 1;
+            const bool ok = blk < nblk && r >= a.alo && r < a.ahi;
+            const Tin *p = in + ((int64_t)r - a.xa0) * rstride + (int64_t)b * V + v0 + vb;
+            if constexpr (sizeof(Tin) == 4) {
+                ld[i] = ok ? __ldcs(reinterpret_cast<const int4 *>(p)) : make_int4(0, 0, 0, 0);
+            } else {
+                ld[i].a = ok ? __ldcs(reinterpret_cast<const longlong2 *>(p)) : make_longlong2(0, 0);
+                ld[i].b = ok ? __ldcs(reinterpret_cast<const longlong2 *>(p) + 1) : make_longlong2(0, 0);
+            }
+        }
+        hw[0] = hw[1] = -1;
+        if (a.hi && blk < nblk) {
+            const int u0 = (int)((v0 & 16383) >> 6);
+            const int P0 = c_y1_uoff[u0], P1 = u0 + 16 < 256 ? c_y1_uoff[u0 + 16] : LRE_Y1_EXC;
 #pragma unroll
-            for (int b = 0; b < 2; ++b) {
-                const bool ok = r >= a.alo && r < a.ahi;
-                const Tin *p = in + ((int64_t)r - a.xa0) * rstride + (int64_t)b * V + v0 + vb;
-                if constexpr (sizeof(Tin) == 4) {
-                    const int4 q = ok ? __ldcs(reinterpret_cast<const int4 *>(p)) : make_int4(0, 0, 0, 0);
-                    x[2 * r + b][0] = (Ta)q.x;
-                    x[2 * r + b][1] = (Ta)q.y;
-                    x[2 * r + b][2] = (Ta)q.z;
-                    x[2 * r + b][3] = (Ta)q.w;
-                } else {
-                    const longlong2 q0 = ok ? __ldcs(reinterpret_cast<const longlong2 *>(p)) : make_longlong2(0, 0);
-                    const longlong2 q1 = ok ? __ldcs(reinterpret_cast<const longlong2 *>(p) + 1) : make_longlong2(0, 0);
-                    x[2 * r + b][0] = (Ta)q0.x;
-                    x[2 * r + b][1] = (Ta)q0.y;
-                    x[2 * r + b][2] = (Ta)q1.x;
-                    x[2 * r + b][3] = (Ta)q1.y;
+            for (int k = 0; k < 2; ++k) {
+                const int p = P0 + (int)threadIdx.x + 256 * k;
+                if (p < P1) {
+                    hw[k] = (int)g_y1_exc_v[p] - (u0 << 6);
+                    const int64_t hrow = ((v0 >> 14) << 11) + p;
+#pragma unroll
+                    for (int i = 0; i < 6; ++i) {
+                        const int r = i >> 1, b = i & 1;
+                        hx[k][i] = (r >= a.alo && r < a.ahi)
+                                       ? __ldg(a.hi + (((int64_t)r - a.xa0) * a.ncol + b) * (V >> 3) + hrow)
+                                       : 0;
+                    }
                 }
             }
-        if (a.hi && (hpos.x & hpos.y) != 0xFFFFFFFFu) {
-            const uint32_t hp[4] = {hpos.x & 0xFFFF, hpos.x >> 16, hpos.y & 0xFFFF, hpos.y >> 16};
-            const int64_t hrow = (((v0 + vb) >> 14) << 11);
+        }
+    };
+    __syncthreads();
+    load(blockIdx.x);
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        uint32_t mh, ah;  // mask / a bits of qubits 2 .. n-5 (natural_to_ma of the block index)
+        natural_to_ma((uint64_t)blk, mh, ah);
+        Ta x[6][4];
 #pragma unroll
-            for (int r = 0; r < 3; ++r)
-#pragma unroll
-                for (int b = 0; b < 2; ++b) {
-                    if (r < a.alo || r >= a.ahi) continue;
-                    const int32_t *h = a.hi + (((int64_t)r - a.xa0) * a.ncol + b) * (V >> 3) + hrow;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        if (hp[e] != 0xFFFF) x[2 * r + b][e] += (Ta)65536 * (Ta)__ldg(h + hp[e]);
-                }
+        for (int i = 0; i < 6; ++i) {
+            if constexpr (sizeof(Tin) == 4) {
+                x[i][0] = (Ta)ld[i].x;
+                x[i][1] = (Ta)ld[i].y;
+                x[i][2] = (Ta)ld[i].z;
+                x[i][3] = (Ta)ld[i].w;
+            } else {
+                x[i][0] = (Ta)ld[i].a.x;
+                x[i][1] = (Ta)ld[i].a.y;
+                x[i][2] = (Ta)ld[i].b.x;
+                x[i][3] = (Ta)ld[i].b.y;
+            }
         }
         uint32_t mt4, at4;  // qubits above the lowest of v = vb + e
         natural_to_ma((uint64_t)threadIdx.x, mt4, at4);
@@ -1689,20 +1712,25 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
             // lowest qubit digit e = I, X, Y, Z -> (m, a) bits (0,0), (1,0), (1,1), (0,1)
             const uint32_t m5 = (mt4 << 1) | (uint32_t)(e == 1 || e == 2), a5 = (at4 << 1) | (uint32_t)(e >= 2);
 #pragma unroll
-            for (int d = 0; d < 4; ++d) {
-                double val;
-                if constexpr (NUM) {
-                    val = __longlong_as_double((long long)D[d]);
-                } else {
-                    const uint32_t mt = (d == 1 || d == 2), at = (d >= 2);
-                    const uint32_t mfull = (mt << (n - 1)) | (mh << 5) | m5, afull = (at << (n - 1)) | (ah << 5) | a5;
-                    val = (double)D[d] * sfac[n - __popc(mfull | afull)];
-                }
-                st[(d * 32 + m5) * 33 + a5] = val;
-            }
+            for (int d = 0; d < 4; ++d) st[(d * 32 + m5) * 33 + a5] = (int64_t)D[d];
         }
         __syncthreads();
-        // 128 rows (digit, m5) of 32 doubles: warp w writes rows w, w + 8, ...
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            if (hw[k] < 0) continue;  // exception: numerator += 65536 * (the same fold of the high parts)
+            const int *h = hx[k];
+            const int64_t H[4] = {(int64_t)h[0] + h[1] + h[2] + h[3] + h[4] + h[5], (int64_t)h[0] - h[1],
+                                  (int64_t)h[2] - h[3], (int64_t)h[4] - h[5]};
+            uint32_t mt, at;
+            natural_to_ma((uint64_t)(hw[k] >> 2), mt, at);
+            const int e = hw[k] & 3;
+            const uint32_t m5 = (mt << 1) | (uint32_t)(e == 1 || e == 2), a5 = (at << 1) | (uint32_t)(e >= 2);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) st[(d * 32 + m5) * 33 + a5] += 65536 * H[d];
+        }
+        __syncthreads();
+        load(blk + gridDim.x);  // in flight during the write-out
+        // 128 rows (digit, m5) of 32 values: warp w writes rows w, w + 8, ...
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll 4
         for (int row = warp; row < 128; row += 8) {
@@ -1710,10 +1738,10 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
             const uint64_t mt = (d == 1 || d == 2), at = (d >= 2);
             const uint64_t m = (mt << (n - 1)) | ((uint64_t)mh << 5) | (uint64_t)m5;
             const uint64_t aa = (at << (n - 1)) | ((uint64_t)ah << 5) | (uint64_t)lane;
-            const double val = st[row * 33 + lane];
+            const int64_t N = st[row * 33 + lane];
             const uint64_t pos = (mask_position(m, n, a.f.layout) << n) | aa;
-            if constexpr (NUM) reinterpret_cast<int64_t *>(a.f.out)[pos] = (int64_t)__double_as_longlong(val);
-            else __stcs(reinterpret_cast<double *>(a.f.out) + pos, val);
+            if constexpr (NUM) reinterpret_cast<int64_t *>(a.f.out)[pos] = N;
+            else __stcs(reinterpret_cast<double *>(a.f.out) + pos, (double)N * sfac[n - __popcll(m | aa)]);
         }
         __syncthreads();
     }
