@@ -729,7 +729,12 @@ def run_dist(args, rank: int, world: int, local: int):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    # keep stdout to the one JSON line: native libraries (the NCCL version banner) write
+    # to fd 1 directly, so fd 1 points at stderr until the line is printed
+    sys.stdout.flush()
+    stdout_fd = os.dup(1)
+    os.dup2(2, 1)
     dist.init_process_group("nccl", device_id=dev)
     n, shots, seed = args.n, args.shots, args.seed
     q = int(_lib.load().lre_shard_quantum(n))
@@ -810,6 +815,9 @@ def run_dist(args, rank: int, world: int, local: int):
         except Exception as exc:
             e2e = {"value": None, "unit": "s", "error": f"{type(exc).__name__}: {str(exc)[:200]}"}
 
+    sys.stdout.flush()
+    os.dup2(stdout_fd, 1)
+    os.close(stdout_fd)
     if rank == 0:
         b = algorithmic_bytes(n, c)
         print(json.dumps({
@@ -838,7 +846,7 @@ def run_dist(args, rank: int, world: int, local: int):
                          "measured_on_hardware": world > 1},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
-        }))
+        }), flush=True)
     dist.destroy_process_group()
 
 

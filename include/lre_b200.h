@@ -88,6 +88,11 @@ int lre_step1_workspace(int n, int64_t shots, int64_t w_begin, int64_t w_end, si
  * Replaces reference pipeline.py:116-138 (step_one_least_squares) together
  * with _kernels.py:34-56 (accumulate_fast) and pauli.py:153-209.
  * w_begin/w_end must be multiples of lre_shard_quantum(n) (except w_end = 3^n).
+ * Contract (as in the reference's MeasurementRecord.validate, records.py:34-56):
+ * every row sums to `shots` and no count is negative.  The integer passes size
+ * their intermediates from that bound (int16 Y1 low halves when shots*27 <=
+ * 32767, int32 while shots*3^q < 2^31); lre_validate_counts checks it on the
+ * device.
  */
 int lre_step1(const void *counts, int count_dtype, int n, int64_t shots, int64_t w_begin,
               int64_t w_end, void *workspace, size_t workspace_bytes, void *out, int out_kind,

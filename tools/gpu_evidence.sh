@@ -22,6 +22,10 @@ if [ -z "$SKIP_NCU" ]; then
   for k in ${NCU_KERNELS:-assemble_x8 final_mm tile_pass}; do
     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
       -o $O/${T}_full_n14_$k -f python bench.py --qubits 14 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-step3 > $O/${T}_ncu_full_$k.log 2>&1
+    # summaries travel back; the reports (tens of MB each) only with KEEP_REP=1
+    python tools/ncu_summary.py $O/${T}_full_n14_$k.ncu-rep > $O/${T}_ncu_full_n14_$k.txt 2>&1
+    python tools/ncu_lines.py $O/${T}_full_n14_$k.ncu-rep 30 > $O/${T}_ncu_lines_n14_$k.txt 2>&1
+    [ -n "$KEEP_REP" ] || rm -f $O/${T}_full_n14_$k.ncu-rep
   done
 fi
 tail -2 $O/${T}_smoke.log $O/${T}_pytest_gpu.log 2>/dev/null
