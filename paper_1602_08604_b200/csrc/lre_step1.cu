@@ -38,6 +38,8 @@
 namespace lre {
 
 #include "lre_y1rank.inc"
+// split Y1 high-part rows: the 1156 used positions padded to a multiple of 32 lanes
+static constexpr int LRE_Y1_HROW = 1184;
 
 // ===========================================================================
 // epilogue shared by both kernels
@@ -130,7 +132,7 @@ struct P1Args {
     int debug_no_l1;
     // split Y1 (Q = 7, SMALL): every value's low 16 bits in lo[tile][16384] (int16), and for the
     // 1156 indices with >= 4 identity digits (the only ones that can exceed int16) the high part
-    // in hi[tile][2048] at their rank; f.out unused
+    // in hi[tile][1184] at their position; f.out unused
     int split16;
     int16_t *lo;
     int16_t *hi;
@@ -416,7 +418,7 @@ __device__ __forceinline__ void l2_subtile_rb(const P1Args &a, const SubTile &st
     // split Y1 (make_plan): the value at u * 64 + dlo (u = top, D1, D2, D3) has a high part
     // iff zc(dlo) >= 4 - zc(u); ZC_U is known at compile time, so most stores need no test.
     int16_t *lo = a.lo + (tile << 14) + dlo;
-    int16_t *hi = a.hi + (tile << 11);
+    int16_t *hi = a.hi + tile * LRE_Y1_HROW;
     const uint32_t lrpack = (Q == 7 && a.split16) ? g_y1_lrpack[dlo] : 0u;
     auto put = [&](int idx_hi, auto zc_u, int32_t val) {  // idx_hi = u * 64
         constexpr int T = 4 - decltype(zc_u)::value;
@@ -980,7 +982,7 @@ struct VArgs {
     int logV, lognB;  // V and nB are powers of two: index math by shifts (64-bit div/mod is ~100 instructions)
     int vf1_batch;  // Q = 1: issue all row loads of 4 elements first (LRE_VF1=0 disables; A/B only)
     Final f;
-    const int32_t *hi = nullptr;  // split Y1 high parts of the input (rows of V / 8) for the fused merge, or null
+    const int32_t *hi = nullptr;  // split Y1 high parts of the input (rows of V / 16384 * 1184) for the merge, or null
 };
 
 // final-store value: integers widen to int64 numerators, fp64 stays fp64
@@ -1198,8 +1200,14 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const 
 
     auto task_coords = [&](int i, int64_t &A, int64_t &B, int64_t &v0) {
         const int64_t t = gw + (int64_t)i * nw;
-        v0 = (t & (nvb - 1)) << 5;
-        const int64_t rest = t >> (a.logV - 5);
+        int64_t rest;
+        if (a.logV >= 0) {
+            v0 = (t & (nvb - 1)) << 5;
+            rest = t >> (a.logV - 5);
+        } else {  // V not a power of two (split-Y1 high-part rows): one division per task
+            rest = t / nvb;
+            v0 = (t - rest * nvb) << 5;
+        }
         B = rest & (a.nB - 1);
         A = a.A0 + (rest >> a.lognB);
     };
@@ -1341,7 +1349,7 @@ struct Plan {
 // every value with zc <= 3 fits int16, so Y1 is stored as an int16 plane of
 // low halves (lo, 2 B per value) plus, for the 1156 of 16384 indices per tile
 // with zc >= 4, the high part hi = (y - lo) / 65536 in a compact int16 plane
-// [tile][2048] (lre_y1rank.inc).  Both planes go through the same Q = 3 folds
+// [tile][1184] (lre_y1rank.inc).  Both planes go through the same Q = 3 folds
 // (linear, so lo and hi chains stay exact: lo after L levels is bounded by
 // 3^L * 32768), and y1_merge_kernel recombines lo + 65536 * hi at the level
 // the final pass reads.  Pass 1 writes and pass 2 reads 10.3 GB instead of
@@ -1419,7 +1427,7 @@ Plan make_plan(int n, int64_t shots, int dtype, int64_t w_begin, int64_t w_end) 
                 const size_t eb = i == 0 ? 2 : 4;  // int16 Y1, int32 later levels
                 const size_t elems = pl.p[i].out_bytes / 4;
                 pl.p[i].hi_off = (elems * eb + 255) & ~(size_t)255;
-                pl.p[i].out_bytes = pl.p[i].hi_off + elems / 8 * eb;
+                pl.p[i].out_bytes = pl.p[i].hi_off + elems / 16384 * LRE_Y1_HROW * eb;
             }
         }
     }
@@ -1671,12 +1679,12 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
                 const int p = P0 + (int)threadIdx.x + 256 * k;
                 if (p < P1) {
                     hw[k] = (int)g_y1_exc_v[p] - (u0 << 6);
-                    const int64_t hrow = ((v0 >> 14) << 11) + p;
+                    const int64_t hrow = (v0 >> 14) * LRE_Y1_HROW + p;
 #pragma unroll
                     for (int i = 0; i < 6; ++i) {
                         const int r = i >> 1, b = i & 1;
                         hx[k][i] = (r >= a.alo && r < a.ahi)
-                                       ? __ldg(a.hi + (((int64_t)r - a.xa0) * a.ncol + b) * (V >> 3) + hrow)
+                                       ? __ldg(a.hi + (((int64_t)r - a.xa0) * a.ncol + b) * ((V >> 14) * LRE_Y1_HROW) + hrow)
                                        : 0;
                     }
                 }
@@ -1688,14 +1696,14 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
     for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         uint32_t mh, ah;  // mask / a bits of qubits 2 .. n-5 (natural_to_ma of the block index)
         natural_to_ma((uint64_t)blk, mh, ah);
-        Ta x[6][4];
+        Tin x[6][4];  // widened to Ta in the fold below
 #pragma unroll
         for (int i = 0; i < 6; ++i) {
             if constexpr (sizeof(Tin) == 4) {
-                x[i][0] = (Ta)ld[i].x;
-                x[i][1] = (Ta)ld[i].y;
-                x[i][2] = (Ta)ld[i].z;
-                x[i][3] = (Ta)ld[i].w;
+                x[i][0] = ld[i].x;
+                x[i][1] = ld[i].y;
+                x[i][2] = ld[i].z;
+                x[i][3] = ld[i].w;
             } else {
                 x[i][0] = (Ta)ld[i].a.x;
                 x[i][1] = (Ta)ld[i].a.y;
@@ -1707,8 +1715,8 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
         natural_to_ma((uint64_t)threadIdx.x, mt4, at4);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            const Ta D[4] = {(x[0][e] + x[1][e]) + (x[2][e] + x[3][e]) + (x[4][e] + x[5][e]), x[0][e] - x[1][e],
-                             x[2][e] - x[3][e], x[4][e] - x[5][e]};
+            const Ta D[4] = {((Ta)x[0][e] + (Ta)x[1][e]) + ((Ta)x[2][e] + (Ta)x[3][e]) + ((Ta)x[4][e] + (Ta)x[5][e]),
+                             (Ta)x[0][e] - (Ta)x[1][e], (Ta)x[2][e] - (Ta)x[3][e], (Ta)x[4][e] - (Ta)x[5][e]};
             // lowest qubit digit e = I, X, Y, Z -> (m, a) bits (0,0), (1,0), (1,1), (0,1)
             const uint32_t m5 = (mt4 << 1) | (uint32_t)(e == 1 || e == 2), a5 = (at4 << 1) | (uint32_t)(e >= 2);
 #pragma unroll
@@ -1808,7 +1816,7 @@ __global__ void __launch_bounds__(256) y1_merge_kernel(int32_t *__restrict__ lo,
         const int64_t h = rem / LRE_Y1_EXC;
         const int rk = (int)(rem - h * LRE_Y1_EXC);
         int32_t *p = lo + row * V + (h << 14) + g_y1_exc_v[rk];
-        const int64_t y = (int64_t)*p + 65536 * (int64_t)hi[row * (V >> 3) + (h << 11) + rk];
+        const int64_t y = (int64_t)*p + 65536 * (int64_t)hi[row * ((V >> 14) * LRE_Y1_HROW) + h * LRE_Y1_HROW + rk];
         *p = (int32_t)y;
     }
 }
@@ -1899,14 +1907,14 @@ static int run_passes(const Plan &pl, const Plan &lay, size_t first, size_t last
             if (fmm && lay.split)  // merge of the split high parts fused into the final pass
                 a.hi = reinterpret_cast<const int32_t *>((const char *)in + lay.p[i - 1].hi_off);
             if (lay.split && !fin) {
-                // lo plane (int16 Y1 at pass 2), then the hi plane: V / 8 lanes per row
+                // lo plane (int16 Y1 at pass 2), then the hi plane: V / 16384 * 1184 lanes per row
                 e = i == 1 ? launch_vfold3<int16_t>(a, stream) : launch_vfold3<int32_t>(a, stream);
                 if (e == cudaSuccess) {
                     VArgs h = a;
                     h.in = (const char *)in + lay.p[i - 1].hi_off;
                     h.f.out = (char *)f.out + ls.hi_off;
-                    h.V = a.V / 8;
-                    h.logV = a.logV - 3;
+                    h.V = a.V / 16384 * LRE_Y1_HROW;
+                    h.logV = -1;  // not a power of two
                     e = i == 1 ? launch_vfold3<int16_t>(h, stream) : launch_vfold3<int32_t>(h, stream);
                 }
                 if (e == cudaSuccess && i + 2 == pl.p.size() && !final_fuses_merge(pl, i + 1, layout, n, done + ps.q)) {

@@ -53,9 +53,9 @@ def test_host_only_entry_points():
 
     ws = ctypes.c_size_t(0)
     assert lib.lre_step1_workspace(14, 1000, 0, 3**14, ctypes.byref(ws)) == _lib.LRE_OK
-    # split Y1 storage (lre_step1.cu make_plan): int16 low halves + a 1/8-size high-part plane
+    # split Y1 storage (lre_step1.cu make_plan): int16 low halves + high-part rows of 1184 per 16384
     e1, e2 = 4**7 * 3**7 * 2**7, 4**10 * 3**4 * 2**4
-    y1, y2 = (e1 + e1 // 8) * 2, (e2 + e2 // 8) * 4
+    y1, y2 = (e1 + e1 // 16384 * 1184) * 2, (e2 + e2 // 16384 * 1184) * 4
     if os.environ.get("LRE_Y1SPLIT") == "0":
         y1, y2 = e1 * 4, e2 * 4
     assert ws.value >= y1 + y2 and ws.value < y1 + y2 + 4096
