@@ -1236,17 +1236,16 @@ __global__ void __launch_bounds__(32 * VF3_WARPS, VF3_MINB) vfold3_kernel(const 
 #pragma unroll
     for (int k = 0; k < VF3_SLOTS; ++k) issue(k);
     int32_t Iacc[16];
-    // int16 input: a task's lines are 64-byte halves of 128-byte lines whose other halves
-    // belong to the neighbouring warp's task.  Keep the CTA's warps in step (one named
-    // barrier per task while every warp still has one) so both halves are requested
-    // together: warps that drift apart re-fetch whole lines from DRAM (measured at n = 14:
-    // up to 2x the reads; with the barrier pass 2 reads 9.17 GB in 2.1 ms instead of 2.6 ms)
+    // Keep the CTA's warps in step: one named barrier per task while every warp still has
+    // one.  With int16 input a task's lines are 64-byte halves of 128-byte lines whose other
+    // halves belong to the neighbouring warp's task; warps that drift apart re-fetch whole
+    // lines from DRAM (n = 14: up to 2x the reads; with the barrier pass 2 reads 9.17 GB in
+    // 2.17 ms instead of 2.6 ms).  int32 passes gain too (n = 14 pass 3: 1.21 -> 1.10 ms):
+    // the CTA's eight tasks stay on neighbouring lines of the same rows.
     const int64_t gw_last = (int64_t)blockIdx.x * VF3_WARPS + VF3_WARPS - 1;
     const int cta_tasks = gw_last < ntask ? (int)((ntask - 1 - gw_last) / nw) + 1 : 0;
     for (int q = 0; q < nq; ++q) {
-        if constexpr (sizeof(Tin) == 2) {
-            if (q % 3 == 0 && q / 3 < cta_tasks) asm volatile("bar.sync 1, %0;" ::"n"(32 * VF3_WARPS) : "memory");
-        }
+        if (q % 3 == 0 && q / 3 < cta_tasks) asm volatile("bar.sync 1, %0;" ::"n"(32 * VF3_WARPS) : "memory");
         const int r1 = q % 3;
         int64_t A, B, v0;
         task_coords(q / 3, A, B, v0);
@@ -1755,14 +1754,20 @@ __global__ void __launch_bounds__(256) final_mm_kernel(const VArgs a) {
     }
 }
 
-static cudaError_t launch_final_mm(int in_dtype, int acc64, const VArgs &a, cudaStream_t s) {
+template <typename Tin, typename Ta, bool NUM> static void launch_fmm_t(const VArgs &a, cudaStream_t s) {
     const int64_t nblk = a.V >> 10;
-    const unsigned grid = (unsigned)std::min<int64_t>(nblk, (int64_t)num_sms() * 8);
+    // 64 blocks per SM (about 7 loop iterations each at n = 14): ncu sweep of blocks per SM
+    // 4 / 8 / 16 / 32 / 64 / 128 / 443 -> 0.86 / 0.83 / 0.79 / 0.77 / 0.755 / 0.754 / 0.81 ms
+    const unsigned grid = (unsigned)std::min<int64_t>(nblk, (int64_t)num_sms() * 64);
+    final_mm_kernel<Tin, Ta, NUM><<<grid, 256, 0, s>>>(a);
+}
+
+static cudaError_t launch_final_mm(int in_dtype, int acc64, const VArgs &a, cudaStream_t s) {
     const bool num = a.f.kind == OUT_NUM;
 #define LRE_FMM(TIN, TA)                                                                  \
     do {                                                                                  \
-        if (num) final_mm_kernel<TIN, TA, true><<<grid, 256, 0, s>>>(a);                  \
-        else final_mm_kernel<TIN, TA, false><<<grid, 256, 0, s>>>(a);                     \
+        if (num) launch_fmm_t<TIN, TA, true>(a, s);                                       \
+        else launch_fmm_t<TIN, TA, false>(a, s);                                          \
     } while (0)
     if (in_dtype == LRE_I32 && acc64) LRE_FMM(int32_t, int64_t);
     else if (in_dtype == LRE_I32) LRE_FMM(int32_t, int32_t);
