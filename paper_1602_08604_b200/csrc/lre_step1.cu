@@ -406,7 +406,9 @@ __device__ __forceinline__ SubTile subtile_of(const P1Args &a, int s) {
 // Q = 7 top qubit (r1, b1) in the thread's private smem slabs tmp / oi.
 // (R1, B1) are compile-time so the per-value top-qubit combine is branch-free
 // (the runtime form spent ~13% of the L2 warps' instructions on branches).
-template <int Q, bool SMALL, int R1, int B1>
+// SPL: split Y1 storage (make_plan) as a compile-time switch: a runtime test per
+// stored value cost the latency-bound L2 warps whole milliseconds of pass 1.
+template <int Q, bool SMALL, int R1, int B1, bool SPL>
 __device__ __forceinline__ void l2_subtile_rb(const P1Args &a, const SubTile &st,
                                               const typename Stage<SMALL>::T *stage, int col, int32_t *tmp,
                                               int32_t *oi) {
@@ -419,10 +421,10 @@ __device__ __forceinline__ void l2_subtile_rb(const P1Args &a, const SubTile &st
     // iff zc(dlo) >= 4 - zc(u); ZC_U is known at compile time, so most stores need no test.
     int16_t *lo = a.lo + (tile << 14) + dlo;
     int16_t *hi = a.hi + tile * LRE_Y1_HROW;
-    const uint32_t lrpack = (Q == 7 && a.split16) ? g_y1_lrpack[dlo] : 0u;
+    const uint32_t lrpack = (Q == 7 && SPL) ? g_y1_lrpack[dlo] : 0u;
     auto put = [&](int idx_hi, auto zc_u, int32_t val) {  // idx_hi = u * 64
         constexpr int T = 4 - decltype(zc_u)::value;
-        if (Q != 7 || !a.split16) {
+        if constexpr (Q != 7 || !SPL) {
             out[idx_hi] = val;
         } else {
             const int16_t l16 = (int16_t)val;
@@ -461,19 +463,19 @@ __device__ __forceinline__ void l2_subtile_rb(const P1Args &a, const SubTile &st
     });
 }
 
-template <int Q, bool SMALL>
+template <int Q, bool SMALL, bool SPL>
 __device__ __forceinline__ void l2_subtile(const P1Args &a, const SubTile &st, const typename Stage<SMALL>::T *stage,
                                            int col, int32_t *tmp, int32_t *oi) {
     if constexpr (Q == 6) {
-        l2_subtile_rb<Q, SMALL, 0, 0>(a, st, stage, col, tmp, oi);
+        l2_subtile_rb<Q, SMALL, 0, 0, SPL>(a, st, stage, col, tmp, oi);
     } else {
         switch (st.r1 * 2 + st.b1) {
-        case 0: l2_subtile_rb<Q, SMALL, 0, 0>(a, st, stage, col, tmp, oi); break;
-        case 1: l2_subtile_rb<Q, SMALL, 0, 1>(a, st, stage, col, tmp, oi); break;
-        case 2: l2_subtile_rb<Q, SMALL, 1, 0>(a, st, stage, col, tmp, oi); break;
-        case 3: l2_subtile_rb<Q, SMALL, 1, 1>(a, st, stage, col, tmp, oi); break;
-        case 4: l2_subtile_rb<Q, SMALL, 2, 0>(a, st, stage, col, tmp, oi); break;
-        default: l2_subtile_rb<Q, SMALL, 2, 1>(a, st, stage, col, tmp, oi); break;
+        case 0: l2_subtile_rb<Q, SMALL, 0, 0, SPL>(a, st, stage, col, tmp, oi); break;
+        case 1: l2_subtile_rb<Q, SMALL, 0, 1, SPL>(a, st, stage, col, tmp, oi); break;
+        case 2: l2_subtile_rb<Q, SMALL, 1, 0, SPL>(a, st, stage, col, tmp, oi); break;
+        case 3: l2_subtile_rb<Q, SMALL, 1, 1, SPL>(a, st, stage, col, tmp, oi); break;
+        case 4: l2_subtile_rb<Q, SMALL, 2, 0, SPL>(a, st, stage, col, tmp, oi); break;
+        default: l2_subtile_rb<Q, SMALL, 2, 1, SPL>(a, st, stage, col, tmp, oi); break;
         }
     }
 }
@@ -488,7 +490,7 @@ __device__ __forceinline__ void l2_subtile(const P1Args &a, const SubTile &st, c
 // interleave their phases.  LOGN > 0 makes the row length 2^LOGN a
 // compile-time constant so the 27 row loads of an item are [base + imm]
 // (the runtime form costs ~5 integer instructions of address math per load).
-template <int Q, bool SMALL, typename Tin, int LOGN>
+template <int Q, bool SMALL, typename Tin, int LOGN, bool SPL = false>
 __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(const P1Args a) {
     using ST = Stage<SMALL>;
     using T = typename ST::T;
@@ -610,14 +612,14 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
         for (int s = 0; s < S; ++s) {
             mbar_wait(&bars[s & 1], (s >> 1) & 1);
             if (!a.debug_no_l2)
-                l2_subtile<Q, SMALL>(a, subtile_of<Q>(a, s), reinterpret_cast<const T *>(smem + (s & 1) * ST::BYTES),
+                l2_subtile<Q, SMALL, SPL>(a, subtile_of<Q>(a, s), reinterpret_cast<const T *>(smem + (s & 1) * ST::BYTES),
                                      tid - 32 * P1_L1_WARPS, tmp, oi);
             mbar_arrive(&bars[2 + (s & 1)]);
         }
     } else {
         for (int s = 0; s <= S; ++s) {
             if (s > 0 && !a.debug_no_l2)
-                l2_subtile<Q, SMALL>(a, subtile_of<Q>(a, s - 1),
+                l2_subtile<Q, SMALL, SPL>(a, subtile_of<Q>(a, s - 1),
                                      reinterpret_cast<const T *>(smem + ((s - 1) & 1) * ST::BYTES),
                                      tid - 32 * P1_L1_WARPS, tmp, oi);
             p1_step_barrier();
@@ -956,7 +958,7 @@ __global__ void __launch_bounds__(TMA_THREADS, 1) tile_tma_kernel(const P1Args a
                 mbar_arrive(&empty[slot]);
             }
         } else if (s > 0) {
-            l2_subtile<Q, true>(a, subtile_of<Q>(a, s - 1),
+            l2_subtile<Q, true, false>(a, subtile_of<Q>(a, s - 1),
                                 reinterpret_cast<const T *>(stage0 + ((s - 1) & 1) * ST::BYTES),
                                 tid - 32 * TMA_L1_WARPS, tmp, oi);
         }
@@ -1358,7 +1360,7 @@ static bool split_allowed() {
     static const bool on = [] {
         const char *e = getenv("LRE_Y1SPLIT");
         const char *v = getenv("LRE_P1");
-        return !(e && e[0] == '0') && !(v && !strcmp(v, "ring"));
+        return !(e && e[0] == '0') && !(v && (!strcmp(v, "ring") || !strcmp(v, "tma")));
     }();
     return on;
 }
@@ -1460,6 +1462,9 @@ static cudaError_t ensure_init() {
 template <int Q, bool SMALL, typename Tin, int LOGN = 0>
 static cudaError_t launch_tile(const P1Args &a, cudaStream_t s) {
     auto kern = tile_pass_kernel<Q, SMALL, Tin, LOGN>;
+    if constexpr (Q == 7 && SMALL) {
+        if (a.split16) kern = tile_pass_kernel<Q, SMALL, Tin, LOGN, true>;
+    }
     const size_t smem = P1Smem<Q, SMALL>::TOTAL;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
