@@ -421,23 +421,23 @@ __device__ __forceinline__ void l2_subtile_rb(const P1Args &a, const SubTile &st
     // iff zc(dlo) >= 4 - zc(u); ZC_U is known at compile time, so most stores need no test.
     int16_t *lo = a.lo + (tile << 14) + dlo;
     int16_t *hi = a.hi + tile * LRE_Y1_HROW;
+    // per threshold t = 4 - zc(u): this thread's rank among the low digit patterns with
+    // >= t identities (t <= 0: its own dlo), and whether it is one
     const uint32_t lrpack = (Q == 7 && SPL) ? g_y1_lrpack[dlo] : 0u;
+    const int hidx[4] = {dlo, (int)(lrpack & 0xFF), (int)((lrpack >> 8) & 0xFF), (int)((lrpack >> 16) & 0xFF)};
+    const bool hok[4] = {true, hidx[1] != 0xFF, hidx[2] != 0xFF, hidx[3] != 0xFF};
     auto put = [&](int idx_hi, auto zc_u, int32_t val) {  // idx_hi = u * 64
         constexpr int T = 4 - decltype(zc_u)::value;
         if constexpr (Q != 7 || !SPL) {
             out[idx_hi] = val;
         } else {
-            const int16_t l16 = (int16_t)val;
-            lo[idx_hi] = l16;
+            lo[idx_hi] = (int16_t)val;
             if constexpr (T < 4) {
-                const int h16 = (val - (int32_t)l16) >> 16;
-                const int uoff = c_y1_uoff[idx_hi >> 6];
-                if constexpr (T <= 0) {
-                    hi[uoff + dlo] = (int16_t)h16;
-                } else {
-                    const int lr = (lrpack >> (8 * (T - 1))) & 0xFF;
-                    if (lr != 0xFF) hi[uoff + lr] = (int16_t)h16;
-                }
+                constexpr int TI = T < 0 ? 0 : T;
+                // high part = floor((val + 2^15) / 2^16), the carry above the signed low half
+                const int pos = c_y1_uoff[idx_hi >> 6] + hidx[TI];
+                const int16_t h16 = (int16_t)((val + 32768) >> 16);
+                if (hok[TI]) hi[pos] = h16;
             }
         }
     };
