@@ -201,6 +201,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// As mbar_wait, but the waiting threads are suspended (up to `hint_ns` per try) instead of
+// spinning: for a producer that waits on a slower consumer, whose warps need the issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t hint_ns) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LRE_WAITS_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra LRE_WAITS_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+}
 // 1-D bulk copy global -> this CTA's shared memory, completing on `bar`
 // (size a multiple of 16 bytes)
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {

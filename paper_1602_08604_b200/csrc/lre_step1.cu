@@ -559,7 +559,8 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
         for (int s = 0; s <= S; ++s) {
             if (a.pipe) {
                 if (s == S) break;
-                if (s >= 2) mbar_wait(&bars[2 + (s & 1)], ((s >> 1) - 1) & 1);
+                // the L2 warps set the pace: sleep instead of spinning on their issue slots
+                if (s >= 2) mbar_wait_sleep(&bars[2 + (s & 1)], ((s >> 1) - 1) & 1, 100000);
             }
             if (s < S && l1 && !a.debug_no_l1) {
                 T *rec = reinterpret_cast<T *>(smem + (s & 1) * ST::BYTES) + tid * STRIDE;
