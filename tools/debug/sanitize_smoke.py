@@ -4,6 +4,10 @@
 Round 2 adds: the 8-CTA-cluster assembly (n = 11: SPLIT and FULL mask blocks,
 whole range and chunked slabs), the mask-major final pass, the fp64 frequency
 folds (device probabilities and a host-streamed source), one-pass streaming.
+Later in round 2: split Y1 storage at n = 11 (the compile-time split tile-pass
+variant with its mbarrier hand-off, the int16 vector pass with its per-task
+barrier, the high-part chain on 1184-entry rows, the final pass's cooperative
+merge, and the natural-layout merge kernel).
 Set LRE_ASM=legacy to route mask-major assembly through the round-1 kernels."""
 import sys
 
@@ -46,6 +50,17 @@ def main():
 
     comp = D.DeviceCompute(11, 40, 0, 3**11, 1, 0, torch.device("cuda", 0), chunks=4)
     D.LocalShardedLRE([comp]).step([rec.counts], rec.lre_dtype)
+    # split Y1 with natural-layout int64 numerators (the separate merge kernel)
+    import ctypes
+
+    from paper_1602_08604_b200 import _lib
+
+    ws = ctypes.c_size_t(0)
+    _lib.check(_lib.load().lre_step1_workspace(11, 40, 0, 3**11, ctypes.byref(ws)), "ws")
+    buf = torch.empty(ws.value, dtype=torch.uint8, device="cuda")
+    num = torch.empty(4**11, dtype=torch.int64, device="cuda")
+    _lib.call("lre_step1", rec.counts.data_ptr(), rec.lre_dtype, 11, 40, 0, 3**11, buf.data_ptr(), ws.value,
+              num.data_ptr(), _lib.OUT_NUM_I64, _lib.NATURAL, torch.cuda.current_stream().cuda_stream)
     # fp64 frequency sources: device probabilities and a host-streamed duck source
     lre.reconstruct(lre.ExactFrequencies(lre.StateDescriptor("random", 5, state_seed=7)), project=False)
 
