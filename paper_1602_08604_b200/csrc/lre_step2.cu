@@ -369,6 +369,38 @@ struct X8Args {
     int64_t units;        // masks / 8
     double scale_half;
     double2 *mu;
+    int order;            // 0: FULL-mode blocks first, round-robin (n = 14); 1: plain stride
+};
+
+// zero bits of m0 in [3, n): SPLIT mode needs three
+__device__ __forceinline__ int zero_bits(uint32_t m0, int n) { return __popc(~m0 & (((1u << n) - 1) & ~7u)); }
+
+// The clusters' block schedule at n = 14.  A FULL-mode block (fewer than three
+// common zero bits, 3% of the blocks) costs ~2.5x a SPLIT block, and a plain
+// stride over u hands one cluster nine of them and another none (u mod 15: the
+// slowest cluster ran ~6% over the mean).  So the blocks are dealt out
+// round-robin, the FULL-mode blocks first (pass 0) and then the SPLIT blocks
+// (pass 1), the dealing position carried across the passes: every cluster gets
+// the same number of each kind to within one.
+struct X8Units {
+    int64_t scan, ph, cid, ncl;
+    int pass;
+    __device__ __forceinline__ int64_t take(const X8Args &a, int n) {
+        if (a.order) {  // plain stride
+            const int64_t u = scan ? scan : cid;
+            scan = u + ncl;
+            return u < a.units ? u : a.units;
+        }
+        for (; pass < 2; ++pass, scan = 0) {
+            for (; scan < a.units; ++scan) {
+                if ((zero_bits((uint32_t)(a.m_begin + scan * 8), n) >= 3) != (pass == 1)) continue;
+                const bool mine = ph == cid;
+                if (++ph == ncl) ph = 0;
+                if (mine) return scan++;
+            }
+        }
+        return a.units;
+    }
 };
 
 // three highest zero bits of m0 in [3, n) (b0 < b1 < b2); false if fewer than three
@@ -430,7 +462,8 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
     }
     cluster.sync();  // every CTA's mbarrier is initialised before any remote st.async
 
-    int64_t u = blockIdx.x / 8;
+    X8Units units{0, 0, (int64_t)blockIdx.x / 8, ncl, 0};
+    int64_t u = units.take(a, LOGD), un_next = a.units;
     // the next block's a' pairs are in flight during the write phase: pair 0 in
     // registers, pair 1 in a per-thread shared-memory stage (cp.async, [combination][thread])
     double2 v[8];
@@ -447,7 +480,8 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
     uint32_t parity = 0;
     bool first = true;
     int it_ = 0;
-    for (; u < a.units; u += ncl, parity ^= 1, ++it_) {
+    for (; u < a.units; u = un_next, parity ^= 1, ++it_) {
+        un_next = units.take(a, LOGD);
         const uint32_t m0 = (uint32_t)(a.m_begin + u * 8);
         const int64_t smask = a.S - 1;
         X8_T(0);
@@ -577,7 +611,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
             X8_T(4);
             // ---- next block's theta into registers (in flight during the write phase) ----
             const int cb0 = b0, cb1 = b1, cb2 = b2;
-            const int64_t un = u + ncl;
+            const int64_t un = un_next;
             bool nsplit = false;
             if (un < a.units) {
                 nsplit = split_bits((uint32_t)(a.m_begin + un * 8), LOGD, b0, b1, b2);
@@ -594,18 +628,25 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
             // 128-byte lines (the L1 processes 8 lines, not 32 partial ones)
             const int lane = t & 31, warp = t >> 5;
             const int rr = lane >> 2, w = lane & 3;
-            const int j0 = rr ^ (2 * w), j1 = j0 ^ 1;  // masks of slots 2w, 2w+1 (row & 7 == rr)
-            const double *A0 = F + j0 * EP, *A1 = F + j1 * EP;  // slot s of row r holds mask (r & 7) ^ s
+            // slot s of row r holds mask (r & 7) ^ s.  The lane's slots are 2w, 2w+1; it
+            // loads slot sa = 2w + (w & 1) first so that each load instruction mixes
+            // odd and even slots: the partner-row loads F_j[rp ^ m0c ^ j] (index
+            // (8 g8 ^ m0c) | s) then fall on all 16 bank pairs, 2 wavefronts per
+            // instruction instead of 4 (all four loads are conflict-free).
+            const int sa = 2 * w + (w & 1), sb = sa ^ 1;
+            const int ja = rr ^ sa, jb = rr ^ sb;
+            const bool swp = w & 1;  // slot 2w holds the sb value
+            const double *Aa = F + ja * EP, *Ab = F + jb * EP;
 #pragma unroll 4
             for (int g8 = warp; g8 < E / 8; g8 += NT / 32) {
                 const int rp = 8 * g8 + rr;
                 const uint32_t r = ins3((uint32_t)rp, cb0, cb1, cb2, 0u) | rpat;
-                const double f1a = A0[pad2_32(rp)], f2a = A0[pad2_32(rp ^ (int)(m0c + j0))];
-                const double f1b = A1[pad2_32(rp)], f2b = A1[pad2_32(rp ^ (int)(m0c + j1))];
+                const double f1a = Aa[pad2_32(rp)], f2a = Aa[pad2_32(rp ^ (int)(m0c + ja))];
+                const double f1b = Ab[pad2_32(rp)], f2b = Ab[pad2_32(rp ^ (int)(m0c + jb))];
                 const double2 oa = make_double2(a.scale_half * (f1a + f2a), a.scale_half * (f2a - f1a));
                 const double2 ob = make_double2(a.scale_half * (f1b + f2b), a.scale_half * (f2b - f1b));
                 double2 *dst = a.mu + (int64_t)r * a.S + ((int64_t)(r ^ m0) & smask & ~(int64_t)7) + 2 * w;
-                st256_cs(dst, oa, ob);
+                st256_cs(dst, swp ? ob : oa, swp ? oa : ob);
             }
             split = nsplit;
         } else {
@@ -701,7 +742,7 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
                     st256_cs(dst + 2 * ((rho >> 1) ^ J), sw ? ob : oa, sw ? oa : ob);
                 }
             }
-            const int64_t un = u + ncl;
+            const int64_t un = un_next;
             if (un < a.units) {
                 split = split_bits((uint32_t)(a.m_begin + un * 8), LOGD, b0, b1, b2);
                 if (split) {
@@ -716,23 +757,14 @@ __global__ void __cluster_dims__(8, 1, 1) __launch_bounds__(X8<LOGD>::NT, LOGD >
     if (!first) cluster_wait();  // partners may still read this CTA's shared memory (FULL mode)
 }
 
-template <int LOGD>
-static int launch_x8(const double *theta, int64_t m_begin, int64_t masks, int64_t S, double *mu, cudaStream_t s) {
-    using C = X8<LOGD>;
-    auto kern = assemble_x8_kernel<LOGD>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
+template <typename K>
+static int launch_cluster8(K kern, int nt, size_t smem, const X8Args &a, cudaStream_t s) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return LRE_ECUDA;
-    X8Args a;
-    a.theta = theta;
-    a.m_begin = m_begin;
-    a.S = S;
-    a.units = masks / 8;
-    a.scale_half = 0.5 * pow(2.0, -LOGD / 2.0);
-    a.mu = reinterpret_cast<double2 *>(mu);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(8, 1, 1);
-    cfg.blockDim = dim3(C::NT, 1, 1);
-    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.blockDim = dim3(nt, 1, 1);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr;
     attr.id = cudaLaunchAttributeClusterDimension;
@@ -745,13 +777,34 @@ static int launch_x8(const double *theta, int64_t m_begin, int64_t masks, int64_
     if (cudaOccupancyMaxActiveClusters(&max_clusters, (void *)kern, &cfg) != cudaSuccess || max_clusters < 1)
         max_clusters = std::max(1, num_sms() / 8);
     const int64_t clusters = std::min<int64_t>(a.units, max_clusters);
-    kern<<<(unsigned)(8 * clusters), C::NT, C::SMEM, s>>>(a);
+    kern<<<(unsigned)(8 * clusters), nt, smem, s>>>(a);
     count_launch();
     return cudaGetLastError() == cudaSuccess ? LRE_OK : LRE_ECUDA;
 }
 
+template <int LOGD>
+static int launch_x8(const double *theta, int64_t m_begin, int64_t masks, int64_t S, double *mu, cudaStream_t s) {
+    // FULL-first round-robin at n = 14 only: at n <= 13 blocks are cheap next to the
+    // serial scan of take() and the synchronised FULL start (n = 13 / 12 / 11
+    // measured 6 / 25 / 50% slower than the stride, n = 14 2.6% faster:
+    // profiles/r03_assembly_experiments.txt).  LRE_X8_ORDER=stride|rr overrides (A/B).
+    static const int forced = [] {
+        const char *v = getenv("LRE_X8_ORDER");
+        return !v ? -1 : !strcmp(v, "stride") ? 1 : !strcmp(v, "rr") ? 0 : -1;
+    }();
+    const int order = forced >= 0 ? forced : LOGD >= 14 ? 0 : 1;
+    X8Args a;
+    a.theta = theta;
+    a.m_begin = m_begin;
+    a.S = S;
+    a.units = masks / 8;
+    a.scale_half = 0.5 * pow(2.0, -LOGD / 2.0);
+    a.mu = reinterpret_cast<double2 *>(mu);
+    a.order = order;
+    return launch_cluster8(assemble_x8_kernel<LOGD>, X8<LOGD>::NT, X8<LOGD>::SMEM, a, s);
+}
+
 // the cluster kernel applies to mask-major slices of >= 8 masks at n >= 11
-// (LRE_ASM=legacy selects the round-1 kernels for A/B runs)
 // (LRE_ASM=legacy selects the round-1 kernels for A/B runs)
 static bool use_cl8(int layout, int n, int64_t S) {
     static const bool legacy = [] {

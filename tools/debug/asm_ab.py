@@ -17,5 +17,5 @@ for _ in range(10):
 e1.record(s)
 e1.synchronize()
 t = e0.elapsed_time(e1) / 10 / 1e3
-print(json.dumps({"n": n, "asm": os.environ.get("LRE_ASM", ""),
+print(json.dumps({"n": n, "asm": os.environ.get("LRE_ASM", ""), "order": os.environ.get("LRE_X8_ORDER", ""),
                   "ms": t * 1e3, "TBps": 24 * 4**n / t / 1e12}))
