@@ -581,6 +581,21 @@ __global__ void __launch_bounds__(P1_THREADS, SMALL ? 2 : 1) tile_pass_kernel(co
                                                 y[2][a2][b5], y[3][a2][b5]);
                         if (a3 < 2) load_step(base, a3 + 1, x);
                         else if (next_base) load_step(next_base, 0, x);
+                        // L2 prefetch of the rows two load steps ahead (the register loads above
+                        // run one step ahead): the L1 warps are load-latency bound, and the extra
+                        // lead cut pass 1 at n = 14 from 29.17 to 28.71 ms (3 steps ahead: 30.2 ms;
+                        // profiles/r02d_pass1_prefetch_ab.txt).  Compile-time row length only, so
+                        // the addresses are [base + immediate] and no register is added.
+                        if constexpr (LOGN > 0) {
+                            // (the last sub-tile has no next one: it re-prefetches its own rows)
+                            const Tin *pb = a3 == 0 || !next_base ? base : next_base;
+                            const Tin *pr = pb + (a3 == 0 ? 2 : a3 - 1) * (1 << LOGN);
+                            static_for<9>([&](auto K) {
+                                constexpr int k = decltype(K)::value;
+                                asm volatile("prefetch.global.L2 [%0+%1];" ::"l"(pr),
+                                             "n"(((k / 3) * 9 + (k % 3) * 3) * (1 << LOGN) * (int)sizeof(Tin)));
+                            });
+                        }
                         int32_t v[16];
 #pragma unroll
                         for (int D4 = 0; D4 < 4; ++D4) {
