@@ -787,7 +787,7 @@ static int launch_x8(const double *theta, int64_t m_begin, int64_t masks, int64_
     // FULL-first round-robin at n = 14 only: at n <= 13 blocks are cheap next to the
     // serial scan of take() and the synchronised FULL start (n = 13 / 12 / 11
     // measured 6 / 25 / 50% slower than the stride, n = 14 2.6% faster:
-    // profiles/r03_assembly_experiments.txt).  LRE_X8_ORDER=stride|rr overrides (A/B).
+    // profiles/r02d_assembly_experiments.txt).  LRE_X8_ORDER=stride|rr overrides (A/B).
     static const int forced = [] {
         const char *v = getenv("LRE_X8_ORDER");
         return !v ? -1 : !strcmp(v, "stride") ? 1 : !strcmp(v, "rr") ? 0 : -1;
