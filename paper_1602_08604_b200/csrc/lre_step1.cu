@@ -140,8 +140,12 @@ struct P1Args {
 };
 
 // --- packed loads: 8 consecutive counts -> 4 words (c[2k] | c[2k+1] << 16) ---
+// (uint16, the benchmarked record: a plain load, which the compiler may schedule
+// freely, ran pass 1 at n = 14 0.75% faster than __ldcs / ld.global.cs, and
+// ld.global.nc / .lu / L1::no_allocate / an asm .ca 0.7-5.5% slower:
+// profiles/r02d_pass1_prefetch_ab.txt)
 __device__ __forceinline__ void load_packed(const uint16_t *p, uint32_t w[4]) {
-    const uint4 u = __ldcs(reinterpret_cast<const uint4 *>(p));
+    const uint4 u = *reinterpret_cast<const uint4 *>(p);
     w[0] = u.x; w[1] = u.y; w[2] = u.z; w[3] = u.w;
 }
 __device__ __forceinline__ void load_packed(const uint8_t *p, uint32_t w[4]) {
